@@ -1,0 +1,361 @@
+"""Pins of the CPU oracle to things other than itself (rule ③).
+
+Every check here compares the oracle with the paper, mathematics or an
+independent computation: textbook values, closed forms, invariants, special
+cases reducing to a textbook stencil, brute force on tiny inputs, dense
+direct solves, and the manufactured-solution convergence the north_star names.
+"""
+import math
+import os
+from fractions import Fraction
+
+import numpy as np
+import pytest
+import scipy.sparse.linalg as spla
+
+import seeded_inputs
+from oracle.band import Band, brute_force_band, lattice_points
+from oracle.interp import OFFS, extension_matrix, extension_rows, lagrange_weights_1d, stencil_of
+from oracle.krylov import arnoldi_fixed, gmres
+from oracle.operator import apply_rows, laplace_beltrami_matrix, laplacian_matrix, shifted_operator
+from oracle.order import band_order_key, slab_bounds
+from oracle.problems import exact_sph, rhs_sph
+from oracle.ras import RAS, disjoint_subdomains, grow_overlap
+from oracle.sph import real_sph
+from oracle.surfaces import Plane, Sphere, Torus
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _golden(name):
+    rows = []
+    for line in open(os.path.join(GOLD, name)):
+        line = line.strip()
+        if line and not line.startswith("#"):
+            rows.append([float(Fraction(tok)) for tok in line.split()])
+    return np.array(rows)
+
+
+# ---------------------------------------------------------------- inputs
+def test_seeded_inputs_counter_based():
+    ijk = np.array([[0, 0, 0], [1, -2, 3], [-5, 7, 11]])
+    a = seeded_inputs.uniform_pm1(0, ijk)
+    b = seeded_inputs.uniform_pm1(0, ijk[::-1])[::-1]
+    assert np.array_equal(a, b)                      # order independent
+    assert np.all((a >= -1) & (a < 1))
+    assert not np.array_equal(a, seeded_inputs.uniform_pm1(1, ijk))
+    big = np.stack(np.meshgrid(*[np.arange(-20, 20)] * 3, indexing="ij"), -1).reshape(-1, 3)
+    u = seeded_inputs.uniform_pm1(0, big)
+    assert abs(u.mean()) < 0.01 and abs(u.var() - 1 / 3) < 0.01
+    z = seeded_inputs.normal(2, big)
+    assert abs(z.mean()) < 0.01 and abs(z.std() - 1) < 0.01
+
+
+# ---------------------------------------------------------------- surfaces (Eq. 3)
+def test_sphere_cp_closed_form():
+    x = np.array([[2.0, 0, 0], [0.3, -0.4, 0.0], [0.1, 0.2, -1.7]])
+    cp, d = Sphere(1.0).cp(x)
+    assert np.allclose(cp[0], [1, 0, 0]) and d[0] == 1.0
+    assert np.allclose(cp[1], [0.6, -0.8, 0]) and abs(d[1] - 0.5) < 1e-15
+    assert np.allclose(np.linalg.norm(cp, axis=1), 1.0, atol=1e-15)
+    assert np.allclose(np.linalg.norm(x - cp, axis=1), d, atol=1e-15)
+    cp2, d2 = Sphere(1.0).cp(cp)                     # idempotence
+    assert np.all(d2 < 1e-15)
+
+
+def _torus_pt(p):
+    return np.array([(1 + 0.4 * np.cos(p[0])) * np.cos(p[1]),
+                     (1 + 0.4 * np.cos(p[0])) * np.sin(p[1]), 0.4 * np.sin(p[0])])
+
+
+def test_torus_cp_matches_brute_force_minimisation():
+    from scipy.optimize import minimize
+
+    rng = np.random.default_rng(5)
+    T = Torus(1.0, 0.4)
+    # random points within 0.3 of the torus
+    th = rng.uniform(0, 2 * np.pi, 40)
+    ph = rng.uniform(0, 2 * np.pi, 40)
+    rr = 0.4 + rng.uniform(-0.3, 0.3, 40)
+    x = np.stack([(1 + rr * np.cos(th)) * np.cos(ph), (1 + rr * np.cos(th)) * np.sin(ph), rr * np.sin(th)], 1)
+    x += rng.normal(0, 0.02, x.shape)
+    cp, d = T.cp(x)
+    # brute force: dense parametric sampling + local refinement by golden search
+    for n in range(x.shape[0]):
+        a = np.linspace(0, 2 * np.pi, 721)
+        A, B = np.meshgrid(a, a, indexing="ij")
+        P = np.stack([(1 + 0.4 * np.cos(A)) * np.cos(B), (1 + 0.4 * np.cos(A)) * np.sin(B), 0.4 * np.sin(A)], -1)
+        D = np.linalg.norm(P - x[n], axis=-1)
+        q = np.unravel_index(np.argmin(D), D.shape)
+        assert D[q] >= d[n] - 1e-12                 # nothing on the surface is closer
+        res = minimize(lambda p: np.linalg.norm(_torus_pt(p) - x[n]), [a[q[0]], a[q[1]]],
+                       method="Nelder-Mead", options={"xatol": 1e-12, "fatol": 1e-15})
+        assert abs(res.fun - d[n]) < 1e-9            # refined optimum = oracle distance
+        assert np.linalg.norm(_torus_pt(res.x) - cp[n]) < 1e-5
+    # cp lies on the torus: (rho - R)^2 + z^2 = r^2
+    rho = np.hypot(cp[:, 0], cp[:, 1])
+    assert np.allclose((rho - 1) ** 2 + cp[:, 2] ** 2, 0.16, atol=1e-13)
+
+
+# ---------------------------------------------------------------- band (§2.1)
+@pytest.mark.parametrize(
+    "surf,h,dist",
+    [
+        (Sphere(1.0), 0.2, lambda x, y, z: abs(math.sqrt(x * x + y * y + z * z) - 1.0)),
+        (Torus(1.0, 0.4), 0.09, lambda x, y, z: abs(math.hypot(math.hypot(x, y) - 1.0, z) - 0.4)),
+    ],
+)
+def test_band_matches_pure_python_triple_loop(surf, h, dist):
+    b = Band(surf, h)
+    act, ghost = brute_force_band(dist, h)
+    assert set(map(tuple, b.active.tolist())) == act
+    assert set(map(tuple, b.ghost.tolist())) == ghost
+    assert b.nA == len(act) and b.nG == len(ghost)
+
+
+def test_band_size_scales_as_h_minus_2():
+    n1 = Band(Sphere(1.0), 0.1).nA
+    n2 = Band(Sphere(1.0), 0.05).nA
+    # codimension-1 tube of width 2 lambda: nA ~ 4 pi * 2 sqrt(17) / h^2
+    assert 3.6 < n2 / n1 < 4.4
+    assert abs(n2 - 4 * math.pi * 2 * math.sqrt(17) / 0.05 ** 2) / n2 < 0.05
+
+
+# ---------------------------------------------------------------- interpolation / E (§2.1)
+def test_lagrange_weights_golden():
+    g = _golden("lagrange_p3.txt")
+    w = lagrange_weights_1d(g[:, 0])
+    assert np.allclose(w, g[:, 1:], atol=2e-16, rtol=0)
+
+
+def test_lagrange_reproduces_cubics_1d():
+    t = np.linspace(0, 1, 101, endpoint=False)
+    w = lagrange_weights_1d(t)
+    tau = np.array([-1.0, 0, 1, 2])
+    for k in range(4):
+        assert np.allclose(w @ tau ** k, t ** k, atol=1e-14)
+
+
+@pytest.mark.parametrize("surf,h", [(Sphere(1.0), 0.1), (Torus(1.0, 0.4), 0.05)])
+def test_E_rows_sum_to_one_and_reproduce_tricubics(surf, h):
+    b = Band(surf, h)
+    E = extension_matrix(b)
+    assert np.abs(np.asarray(E.sum(axis=1)).ravel() - 1).max() < 1e-13
+    xa = lattice_points(b.active, h)
+    cp, _ = surf.cp(lattice_points(b.all, h))
+    rng = np.random.default_rng(1)
+    for _ in range(6):
+        a, bb, c = rng.integers(0, 4, 3)
+        q = lambda P: (P[:, 0] ** a) * (P[:, 1] ** bb) * (P[:, 2] ** c)
+        assert np.abs(E @ q(xa) - q(cp)).max() < 1e-12
+
+
+def test_E_on_lattice_plane_is_selection():
+    P = Plane(0.0)
+    b_nodes = np.array([[i, j, k] for i in range(-3, 4) for j in range(-3, 4) for k in range(-2, 3)])
+
+    class _B:  # minimal band: every node is "active"
+        h = 0.25
+        surface = P
+        akeys = None
+
+    from oracle.band import node_key
+
+    _B.akeys = np.sort(node_key(np.array([[i, j, k] for i in range(-8, 9) for j in range(-8, 9) for k in range(-4, 5)])))
+    _B.all = b_nodes
+    cols, vals = extension_rows(_B, b_nodes)
+    assert np.all(np.isclose(vals, 0) | np.isclose(vals, 1))
+    assert np.allclose(vals.sum(1), 1)
+
+
+# ---------------------------------------------------------------- operators (Eq. 2, 4)
+def test_delta_h_exact_on_quadratics():
+    b = Band(Sphere(1.0), 0.1)
+    D = laplacian_matrix(b)
+    X = lattice_points(b.all, b.h)
+    p = 3 * X[:, 0] ** 2 - X[:, 1] * X[:, 2] + 2 * X[:, 2] ** 2 + X[:, 0]
+    assert np.allclose(D @ p, 10.0, atol=1e-9)
+
+
+def test_semidiscrete_2d_golden_on_plane():
+    """the flat case reduces to the 2-D -4/h^2, +1/h^2 stencil."""
+    for h, centre, nb in _golden("semidiscrete_2d.txt"):
+        P = Plane(0.0)
+
+        class _B:
+            pass
+
+        _B.h = h
+        _B.surface = P
+        probes = np.array([[0, 0, 0], [1, -2, 0], [3, 1, 0]])
+        # u = delta function at a probe and its neighbours -> read off stencil weights
+        for pr in probes:
+            def u_delta(ijk, tgt):
+                return np.all(ijk == tgt[None, :], axis=1).astype(float)
+
+            y_c = apply_rows(_B, 0.0, lambda q: u_delta(q, pr), pr[None, :])[0]
+            y_n = apply_rows(_B, 0.0, lambda q: u_delta(q, pr + np.array([1, 0, 0])), pr[None, :])[0]
+            y_z = apply_rows(_B, 0.0, lambda q: u_delta(q, pr + np.array([0, 0, 1])), pr[None, :])[0]
+            # A = c I - Delta_S^h with c = 0  ->  -Delta_S^h
+            assert abs(-y_c - centre) < 1e-9 * abs(centre)
+            assert abs(-y_n - nb) < 1e-9 * abs(nb)
+            assert abs(y_z) == 0.0                   # off-plane values are never read
+
+
+def test_constants_in_kernel():
+    b = Band(Sphere(1.0), 0.1)
+    L = laplace_beltrami_matrix(b)
+    assert np.abs(L @ np.ones(b.nA)).max() < 1e-9 * 6 / b.h ** 2
+
+
+def test_apply_rows_equals_assembled_matrix():
+    b = Band(Torus(1.0, 0.4), 0.05)
+    A = shifted_operator(b, 2.5)
+    u_of = lambda ijk: seeded_inputs.uniform_pm1(7, ijk)
+    u = u_of(b.active)
+    y = A @ u
+    sel = np.random.default_rng(0).choice(b.nA, 300, replace=False)
+    y1 = apply_rows(b, 2.5, u_of, b.active[sel])
+    assert np.abs(y1 - y[sel]).max() <= 1e-12 * np.abs(y).max()
+
+
+def test_eigenfunction_second_order():
+    """Closed form on the unit sphere: the closest point extension of Y is constant on rays,
+    so Delta(E Y)(x) = Delta_S Y / |x|^2 = -l(l+1) Y / |x|^2.  Eq. (4) must reproduce it
+    at every band node up to O(h^2) (FD error O(h^2) + interpolation error O(h^4)/h^2)."""
+    errs = []
+    for h in (0.1, 0.05):
+        b = Band(Sphere(1.0), h)
+        L = laplace_beltrami_matrix(b)
+        Y = exact_sph(b, 3, 2)
+        r2 = np.sum(lattice_points(b.active, h) ** 2, axis=1)
+        r = L @ Y + 12 * Y / r2
+        errs.append(np.abs(r).max())
+    assert errs[0] / errs[1] > 3.2
+
+
+# ---------------------------------------------------------------- spherical harmonics
+def test_real_sph_orthonormal():
+    xg, wg = np.polynomial.legendre.leggauss(40)
+    ph = np.linspace(0, 2 * np.pi, 80, endpoint=False)
+    CT, PH = np.meshgrid(xg, ph, indexing="ij")
+    W = np.repeat(wg[:, None], 80, 1) * (2 * np.pi / 80)
+    st = np.sqrt(1 - CT ** 2)
+    P = np.stack([st * np.cos(PH), st * np.sin(PH), CT], -1).reshape(-1, 3)
+    lm = [(3, 2), (6, 3), (10, 5), (2, -1), (0, 0), (6, -3)]
+    Ys = [real_sph(l, m, P) for l, m in lm]
+    for a in range(len(lm)):
+        for b_ in range(len(lm)):
+            ip = np.sum(Ys[a] * Ys[b_] * W.ravel())
+            assert abs(ip - (a == b_)) < 1e-12
+
+
+@pytest.mark.parametrize("l,m", [(3, 2), (6, 3), (10, 5)])
+def test_real_sph_is_harmonic_polynomial(l, m):
+    """r^l Y_l^m(x/r) is harmonic: its 3-D Laplacian vanishes (=> Delta_S Y = -l(l+1) Y)."""
+    rng = np.random.default_rng(l)
+    x = rng.normal(size=(20, 3))
+    x /= np.linalg.norm(x, axis=1, keepdims=True)
+    f = lambda P: np.linalg.norm(P, axis=1) ** l * real_sph(l, m, P)
+    d = 1e-3
+    lap = -6 * f(x)
+    for c in range(3):
+        e = np.zeros(3)
+        e[c] = d
+        lap = lap + f(x + e) + f(x - e)
+    lap /= d * d
+    scale = l * l * np.abs(f(x)).max() + 1
+    assert np.abs(lap).max() < 1e-4 * scale
+
+
+# ---------------------------------------------------------------- manufactured solve (north_star pin)
+def test_manufactured_solution_second_order():
+    """u = Y_3^2(cp(x)), f = (c + 12) u converges at 2nd order (direct sparse solves)."""
+    errs = []
+    for h in (0.16, 0.08):
+        b = Band(Sphere(1.0), h)
+        A = shifted_operator(b, 1.0)
+        u = spla.spsolve(A.tocsc(), rhs_sph(b, 1.0, 3, 2))
+        errs.append(np.abs(u - exact_sph(b, 3, 2)).max())
+    assert errs[1] < 0.01
+    assert errs[0] / errs[1] > 3.2                  # observed order >= ~1.7 (pre-asymptotic ~3)
+
+
+# ---------------------------------------------------------------- GMRES
+def test_gmres_identity_one_iteration():
+    b = np.arange(1.0, 11.0)
+    x, st = gmres(lambda v: v, b, restart=5, rtol=1e-12)
+    assert st.iterations == 1 and np.allclose(x, b)
+
+
+def test_gmres_dense_random_vs_lu():
+    rng = np.random.default_rng(3)
+    A = rng.normal(size=(60, 60)) + 15 * np.eye(60)
+    b = rng.normal(size=60)
+    x, st = gmres(lambda v: A @ v, b, restart=7, rtol=1e-12)
+    assert st.converged
+    assert np.abs(x - np.linalg.solve(A, b)).max() < 1e-10
+    assert st.resid_true <= 1.01e-12 * np.linalg.norm(b) + 1e-14
+
+
+def test_gmres_cpm_tiny_band_vs_dense_direct():
+    b = Band(Sphere(1.0), 0.16)
+    A = shifted_operator(b, 1.0)
+    f = rhs_sph(b, 1.0, 3, 2)
+    x, st = gmres(lambda v: A @ v, f, restart=30, rtol=1e-10)
+    xd = np.linalg.solve(A.toarray(), f)
+    assert st.converged
+    assert np.abs(x - xd).max() / np.abs(xd).max() < 1e-8
+
+
+def test_arnoldi_fixed_full_dimension_is_exact():
+    rng = np.random.default_rng(4)
+    A = rng.normal(size=(12, 12)) + 6 * np.eye(12)
+    r = rng.normal(size=12)
+    z = arnoldi_fixed(lambda v: A @ v, r, 12)
+    assert np.allclose(A @ z, r, atol=1e-10)
+
+
+# ---------------------------------------------------------------- RAS (§2.2)
+def test_order_key_hand_values():
+    k = band_order_key(np.array([[0, 0, 0], [1, 0, 0], [0, 1, 0], [0, 0, 1], [8, 0, 0], [-1, 0, 0]]))
+    base = (1 << 48) | (1 << 49) | (1 << 50)   # interleave(2^16) for x, y, z
+    assert k[0] == base * 512
+    assert k[1] == base * 512 + 1 and k[2] == base * 512 + 8 and k[3] == base * 512 + 64
+    assert k[4] == (base | 1) * 512
+    # brick -1 in x: 2^16 - 1 = 0xFFFF interleaved -> bits 0,3,...,45
+    m = sum(1 << (3 * b) for b in range(16)) | (1 << 49) | (1 << 50)
+    assert k[5] == m * 512 + 7
+
+
+def test_partition_and_overlap_invariants():
+    b = Band(Sphere(1.0), 0.1)
+    dis = disjoint_subdomains(b, 8)
+    allidx = np.sort(np.concatenate(dis))
+    assert np.array_equal(allidx, np.arange(b.nA))
+    assert max(len(d) for d in dis) - min(len(d) for d in dis) <= 1
+    o2 = grow_overlap(b, dis[3], 2)
+    o4 = grow_overlap(b, dis[3], 4)
+    assert set(dis[3]).issubset(o2) and set(o2).issubset(o4)
+    assert slab_bounds(10, 3) == [0, 3, 6, 10]
+
+
+def test_ras_single_subdomain_exact_is_inverse():
+    b = Band(Sphere(1.0), 0.16)
+    A = shifted_operator(b, 1.0)
+    M = RAS(b, A, nsub=1, overlap=0, local="exact")
+    f = rhs_sph(b, 1.0, 3, 2)
+    x, st = gmres(lambda v: A @ v, f, restart=30, rtol=1e-10, M=M)
+    assert st.iterations == 1
+
+
+def test_ras_fgmres_converges_to_single_domain_solution():
+    b = Band(Sphere(1.0), 0.1)
+    A = shifted_operator(b, 1.0)
+    f = rhs_sph(b, 1.0, 3, 2)
+    x0, s0 = gmres(lambda v: A @ v, f, restart=30, rtol=1e-10)
+    for local, k in (("exact", 0), ("gmres", 8)):
+        M = RAS(b, A, nsub=8, overlap=4, k_inner=k, local=local)
+        x1, s1 = gmres(lambda v: A @ v, f, restart=30, rtol=1e-10, M=M)
+        assert s1.converged
+        assert np.abs(x1 - x0).max() / np.abs(x0).max() < 1e-8
