@@ -1,0 +1,345 @@
+#!/usr/bin/env python
+"""bench.py — CPM hot path on B200 (BASELINE.json metric, config 1).
+
+A step is one pass of the hot path over config 1 (BASELINE.json configs[1]):
+unit sphere, h = 1/200 (~4.1M band nodes), fp64:
+  * 100 operator applies y = (c - Delta_S^h) u on u ~ U[-1,1] (seed 0), c = 10
+  * the manufactured solve (c - Delta_S^h) u = (c + 42) Y_6^3(cp), GMRES(50), rtol 1e-10
+`value` = band-node applies per second over the timed applies (CUDA events on the
+launching stream, max over ranks); `solve` reports the GMRES solve time.  The
+band is built once, outside the timed region (its build time is reported).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+N > 1 (torchrun): every rank runs the config on its own GPU ("replicas";
+DESIGN.md §Multi-GPU), value = total applies / max-over-ranks time.
+--impl reference: the CPU oracle (oracle/, the tier's reference arm) on the host
+cores, same config and metric, on a bounded sample of rows per step.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CFG = dict(surface="sphere", R=1.0, h=1.0 / 200, c=10.0, applies=100, l=6, m=3, restart=50,
+           rtol=1e-10)
+WORKLOAD = ("BASELINE configs[1]: unit sphere h=1/200, fp64, 100 applies on U[-1,1] seed 0 "
+            "+ Y_6^3 solve c=10 GMRES(50) rtol 1e-10, 1 GPU")
+METRIC = "CPM apply band-nodes/s"
+UNIT = "band-nodes/s"
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap,power.draw")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.rows = []
+        self.proc = None
+        self.t = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except FileNotFoundError:
+            self.proc = None
+            return
+        self.t = threading.Thread(target=self._read, daemon=True)
+        self.t.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 7:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        if self.t is not None:
+            self.t.join(timeout=2)
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            for nm, v in zip(names, r[3:7]):
+                if v.strip().lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def cpu_oracle_rate(n_rows: int, seed: int = 0):
+    """Oracle (oracle.operator.apply_rows, as it stands) on n_rows sampled band rows of config 1.
+    Returns (rows/s, seconds, threads)."""
+    from oracle.band import lam_of
+    from oracle.operator import apply_rows
+    from oracle.surfaces import Sphere
+    import seeded_inputs
+
+    h = CFG["h"]
+
+    class _B:
+        pass
+
+    _B.h = h
+    _B.surface = Sphere(CFG["R"])
+    # sample lattice nodes inside the lambda-tube by the oracle's own test
+    rng = np.random.default_rng(seed)
+    rows = []
+    got = 0
+    lam = lam_of(h)
+    while got < n_rows:
+        d = rng.normal(size=(2 * n_rows, 3))
+        d /= np.linalg.norm(d, axis=1, keepdims=True)
+        r = CFG["R"] + rng.uniform(-lam, lam, size=(2 * n_rows, 1))
+        ijk = np.round(d * r / h).astype(np.int64)
+        _, dist = _B.surface.cp(ijk.astype(np.float64) * h)
+        ijk = ijk[dist <= lam]
+        rows.append(ijk)
+        got += len(ijk)
+    ijk = np.concatenate(rows)[:n_rows]
+    t0 = time.perf_counter()
+    for s in range(0, n_rows, 8192):
+        apply_rows(_B, CFG["c"], lambda q: seeded_inputs.uniform_pm1(0, q), ijk[s:s + 8192])
+    dt = time.perf_counter() - t0
+    return n_rows / dt, dt, 1
+
+
+def run_reference(args):
+    ws, rank, _ = _dist()
+    if rank != 0:
+        return 0
+    rows = args.ref_rows
+    for _ in range(args.warmup):
+        cpu_oracle_rate(max(rows // 8, 1024))
+    rates, secs = [], []
+    for k in range(args.steps):
+        r, dt, thr = cpu_oracle_rate(rows, seed=k)
+        rates.append(r)
+        secs.append(dt)
+    value = float(np.mean(rates))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * float(np.mean(secs)),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded U[-1,1] per lattice node)",
+        "config": {"workload": WORKLOAD, "sample": f"{rows} oracle rows per step"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                         "sample": f"{rows} sampled active rows of config 1 per step, "
+                                   "oracle.operator.apply_rows (numpy, 1 thread)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_mine(args):
+    import torch
+
+    ws, rank, local = _dist()
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    from paper_2110_06322_b200._build import build
+
+    if rank == 0:
+        build()
+    if ws > 1:
+        torch.distributed.barrier()
+    import paper_2110_06322_b200 as cpm
+    import seeded_inputs
+
+    stream = torch.cuda.current_stream(dev)
+    t0 = time.perf_counter()
+    band = cpm.cpm_build_band(CFG["surface"], CFG["h"], R=CFG["R"])
+    torch.cuda.synchronize()
+    build_s = time.perf_counter() - t0
+    nA, nG = band.info.n_active, band.info.n_ghost
+    nE = nA + nG
+    coords = cpm.cpm_band_active_coords(band).astype(np.int64)
+    u_host = torch.from_numpy(seeded_inputs.uniform_pm1(0, coords)).pin_memory()
+    u = u_host.to(dev, non_blocking=False)
+    y = torch.empty_like(u)
+    f = torch.empty_like(u)
+    cpm.cpm_eval_sph(band, CFG["l"], CFG["m"], CFG["c"] + CFG["l"] * (CFG["l"] + 1), f)
+    x = torch.zeros_like(u)
+    c = CFG["c"]
+
+    def step(record):
+        evs = []
+        for _ in range(CFG["applies"]):
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            cpm.cpm_apply(band, c, u, y)
+            b.record(stream)
+            evs.append((a, b))
+        x.zero_()
+        sa = torch.cuda.Event(enable_timing=True)
+        sb = torch.cuda.Event(enable_timing=True)
+        sa.record(stream)
+        st = cpm.cpm_solve(band, c, f, x, rtol=CFG["rtol"], restart=CFG["restart"])
+        sb.record(stream)
+        if record is not None:
+            record.append((evs, (sa, sb), st))
+
+    for _ in range(args.warmup):
+        step(None)
+    torch.cuda.synchronize()
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    cpm.cpm_profile_reset()
+    cpm.cpm_profile_enable(True)
+    launches0 = cpm.cpm_kernel_launches()
+    rec = []
+    if ws > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    ga = torch.cuda.Event(enable_timing=True)
+    gb = torch.cuda.Event(enable_timing=True)
+    ga.record(stream)
+    for _ in range(args.steps):
+        step(rec)
+    gb.record(stream)
+    torch.cuda.synchronize()
+    if ws > 1:
+        torch.distributed.barrier()
+    launches = cpm.cpm_kernel_launches() - launches0
+    cpm.cpm_profile_enable(False)
+    clk = clocks.stop()
+    total_ms = ga.elapsed_time(gb)
+    apply_ms = sum(a.elapsed_time(b) for evs, _, _ in rec for a, b in evs)
+    solve_ms = [sa.elapsed_time(sb) for _, (sa, sb), _ in rec]
+    stats = [st for _, _, st in rec]
+    ext_ms, ext_n = cpm.cpm_profile_read("extend")
+    lap_ms, lap_n = cpm.cpm_profile_read("laplace")
+    kern = {k: cpm.cpm_profile_read(k) for k in ["mdot", "cgs_update", "cgs_final", "axpy", "other"]}
+
+    # e2e: same metric through the C ABI with HOST buffers (pinned), copies inside the timed region
+    y_host = torch.empty(nA, dtype=torch.float64).pin_memory()
+    u_np, y_np = u_host.numpy(), y_host.numpy()
+    e2e_steps = max(1, min(args.steps, 2))
+    torch.cuda.synchronize()
+    if ws > 1:
+        torch.distributed.barrier()
+    t_e = time.perf_counter()
+    for _ in range(e2e_steps):
+        for _ in range(CFG["applies"]):
+            cpm.cpm_apply(band, c, u_np, y_np)
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - t_e
+
+    # reductions over ranks (max time)
+    vals = torch.tensor([apply_ms, total_ms, e2e_s, float(np.median(solve_ms))], dtype=torch.float64, device=dev)
+    if ws > 1:
+        torch.distributed.all_reduce(vals, op=torch.distributed.ReduceOp.MAX)
+    apply_ms, total_ms, e2e_s, solve_med_ms = [float(v) for v in vals.cpu()]
+    n_applies = CFG["applies"] * args.steps
+    value = ws * nA * n_applies / (apply_ms / 1e3)
+    e2e_value = ws * nA * CFG["applies"] * e2e_steps / e2e_s
+
+    peak, peak_src = _peaks()
+    alg_bytes = 16 * nA + 28 * nE          # u + y + (t_xyz + eoff) per eval node
+    mean_apply_s = (ext_ms + lap_ms) / 1e3 / max(ext_n, 1)
+    achieved = alg_bytes / mean_apply_s / 1e9
+    if rank == 0:
+        cpu_rate, cpu_s, cores = (None, None, None)
+        if not args.no_cpu and ws == 1:
+            cpu_rate, cpu_s, cores = cpu_oracle_rate(args.cpu_rows)
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded U[-1,1] per lattice node; manufactured Y_6^3 rhs)",
+            "config": {"workload": WORKLOAD, "n_active": nA, "n_ghost": nG, "n_tiles": band.info.n_tiles,
+                       "applies_per_step": CFG["applies"], "parallelism": f"replicas x{ws}",
+                       "l2": f"inputs larger than L2: apply working set "
+                             f"{(alg_bytes + band.info.n_tiles * 4096) / 1e6:.0f} MB vs 126 MB L2"},
+            "solve": {"seconds_median": solve_med_ms / 1e3, "iterations": stats[-1].iterations,
+                      "converged": stats[-1].converged, "resid_true_rel": stats[-1].resid_true / stats[-1].bnorm},
+            "build_band_s": build_s,
+            "roofline": {"kernel": "apply = extend + laplace (per apply)", "bound": "hbm",
+                         "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                         "traffic": None, "peak_source": peak_src,
+                         "alg_bytes_per_apply": alg_bytes,
+                         "extend_ms": ext_ms / max(ext_n, 1), "laplace_ms": lap_ms / max(lap_n, 1)},
+            "kernels_ms_total": {"extend": ext_ms, "laplace": lap_ms, **{k: v[0] for k, v in kern.items()}},
+            "cpu_baseline": ({"value": cpu_rate, "unit": UNIT, "cores": cores, "kind": "oracle",
+                              "sample": f"{args.cpu_rows} sampled active rows of config 1, "
+                                        f"oracle.operator.apply_rows, {cpu_s:.1f} s"}
+                             if cpu_rate else None),
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 8 * nA * CFG["applies"],
+                    "d2h_bytes_per_step": 8 * nA * CFG["applies"]},
+            "gpu_launches": launches,
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="mine", choices=["mine", "reference"])
+    ap.add_argument("--cpu-rows", type=int, default=1 << 18)
+    ap.add_argument("--ref-rows", type=int, default=1 << 16)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        print("warning: --warmup < 3 violates the timing rules; using 3", file=sys.stderr)
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_mine(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

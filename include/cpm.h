@@ -1,0 +1,175 @@
+/*
+ * cpm.h — C ABI of the B200-native closest point method (CPM) hot path.
+ *
+ * The operations follow the problem statement of May, Haynes & Ruuth,
+ * "A closest point method library for PDEs on surfaces with parallel domain
+ * decomposition solvers and preconditioners" (arXiv:2110.06322), reproduced in
+ * PAPER.md; "PAPER.md:N" below cites its line N.  DESIGN.md lists the readings
+ * (R1..R12) taken where the paper is silent.
+ *
+ * Conventions (all entry points):
+ *  - Return CPM_OK (0) on success, a negative CPM_ERR_* code otherwise; the
+ *    message of the last error on the calling thread is cpm_last_error().
+ *    No entry point aborts the process.
+ *  - Floating point is IEEE binary64 ("fp64") throughout.
+ *  - Vector arguments are plain pointers to nA doubles (nA = number of active
+ *    nodes) in BAND ORDER (reading R8: Morton order of 8^3 bricks, then z,y,x
+ *    inside a brick).  A pointer may be DEVICE memory (cudaMalloc / torch CUDA
+ *    tensor) or HOST memory (pageable or pinned); host pointers are staged
+ *    through device buffers owned by the band, with the copies on `stream`.
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *    Calls are asynchronous w.r.t. the host for device pointers, except where
+ *    a result must reach the host (cpm_solve statistics, host outputs).
+ *  - Handles (cpm_band, cpm_ras, cpm_comm) are owned by the caller and
+ *    released with the matching *_free; they own all device memory they use.
+ *  - Only p = 3 (tricubic) interpolation and d = 3 are implemented.
+ */
+#ifndef CPM_H_
+#define CPM_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CPM_OK 0
+#define CPM_ERR_ARG (-1)      /* invalid argument */
+#define CPM_ERR_CUDA (-2)     /* CUDA runtime error (message has the CUDA text) */
+#define CPM_ERR_GEOM (-3)     /* closest point undefined in the band / stencil leaves Sigma_A */
+#define CPM_ERR_NOMEM (-4)    /* device or host allocation failed */
+#define CPM_ERR_NCCL (-5)     /* NCCL error (multi-GPU calls) */
+#define CPM_ERR_LIMIT (-6)    /* a size limit of this implementation was exceeded */
+
+/* Surfaces with an analytic closest point function cp_S (Eq. 3). */
+#define CPM_SURF_SPHERE 1 /* param[0] = radius R, centred at the origin */
+#define CPM_SURF_TORUS 2  /* param[0] = major radius R, param[1] = minor radius r, axis z */
+
+typedef struct cpm_surface {
+  int32_t kind;
+  double param[4];
+} cpm_surface;
+
+typedef struct cpm_band cpm_band;
+typedef struct cpm_ras cpm_ras;
+typedef struct cpm_comm cpm_comm;
+
+typedef struct cpm_band_info {
+  int64_t n_active;   /* |Sigma_A| — the unknowns */
+  int64_t n_ghost;    /* |Sigma_G| */
+  int64_t n_tiles;    /* occupied 8^3 bricks (apply work units) */
+  int64_t n_runs;     /* stencil-box fill runs (apply metadata) */
+  int64_t max_box;    /* largest per-tile stencil box, cells */
+  int64_t bytes_device; /* device memory held by the band */
+  double h, lambda, L;
+  int32_t lattice_lo[3], lattice_hi[3]; /* inclusive lattice bounds of Sigma_A u Sigma_G */
+  int32_t zero_fill;  /* 1 if some stencil cell is not a source node (sub-bands) */
+  int32_t rank, nranks; /* owning rank of a partitioned band (0, 1 otherwise) */
+  int64_t n_owned;    /* owned active nodes (== n_active unless partitioned) */
+  int64_t n_halo;     /* halo source nodes received from other ranks */
+} cpm_band_info;
+
+typedef struct cpm_solve_stats {
+  int32_t iterations;  /* Arnoldi steps (operator applications inside cycles) */
+  int32_t converged;   /* 1 if |g_{k+1}| <= rtol ||f|| was reached */
+  int32_t cycles;      /* restart cycles */
+  int32_t breakdown;   /* 1 on happy breakdown */
+  double resid_est;    /* Givens residual estimate at exit */
+  double resid_true;   /* ||f - A u||_2 recomputed at exit */
+  double bnorm;        /* ||f||_2 */
+  double seconds;      /* wall time of the call (host clock, includes syncs) */
+} cpm_solve_stats;
+
+/* ---------------------------------------------------------------- version / errors */
+const char* cpm_version(void);
+const char* cpm_last_error(void);
+
+/* ---------------------------------------------------------------- band construction
+ * cpm_build_band — north_star item (1); PAPER.md:62 (Sigma_A, Sigma_G),
+ * PAPER.md:76 (the (p+1)^d interpolation cubes).
+ *   Sigma_A = { x = h (i,j,k), |i|,|j|,|k| <= round(L/h) : |x - cp(x)| <= lambda },
+ *   lambda = sqrt(17) h (reading R1); Sigma_G = 6-neighbours of Sigma_A outside it.
+ *   For every node of Sigma_A u Sigma_G: cp(x), the stencil base floor(cp/h) - 1
+ *   and the fractional offset cp/h - floor(cp/h) (reading R2), plus the bucketed
+ *   (8^3-brick) node -> lattice map used by the apply.
+ * Arguments: surface (host struct), h > 0 grid spacing, p (must be 3),
+ *   L > 0 half-width of the computational box [-L, L]^3, stream, out (receives
+ *   the handle).  Device work runs on `stream`; the call synchronises it.
+ * Errors: CPM_ERR_ARG (p != 3, h <= 0, unknown surface), CPM_ERR_GEOM (cp
+ *   undefined at a band node or a stencil leaves Sigma_A — the band is wider
+ *   than the surface's reach), CPM_ERR_LIMIT, CPM_ERR_CUDA. */
+int cpm_build_band(const cpm_surface* surface, double h, int p, double L, void* stream,
+                   cpm_band** out);
+int cpm_band_get_info(const cpm_band* band, cpm_band_info* info);
+/* Lattice coordinates (i,j,k) of the active / ghost nodes, in band order, into
+ * a HOST int32 array of 3*n entries. */
+int cpm_band_active_coords(const cpm_band* band, int32_t* ijk_host);
+int cpm_band_ghost_coords(const cpm_band* band, int32_t* ijk_host);
+void cpm_band_free(cpm_band* band);
+
+/* ---------------------------------------------------------------- operator apply
+ * cpm_apply — y = (c I - Delta_S^h) u with Delta_S^h of PAPER.md:80-85 (Eq. 4,
+ * d = 3) and c of Eq. 2:
+ *   y = c u - [ Delta_h E u - (6/h^2)(u - E u) ] = (c + 6/h^2) u - (1/h^2) sum_{6 nbrs} (E u)
+ * E is the tricubic barycentric Lagrange extension, applied
+ * matrix-free: weights are recomputed from the stored fractional offsets.
+ * u, y: nA doubles each (device or host), must not alias.  Asynchronous on
+ * `stream` for device pointers; synchronous for host pointers.
+ * Errors: CPM_ERR_ARG (null pointers / aliasing), CPM_ERR_CUDA. */
+int cpm_apply(const cpm_band* band, double c, const double* u, double* y, void* stream);
+
+/* ---------------------------------------------------------------- Krylov solve
+ * cpm_solve — solve (c - Delta_S^h) u = f (Eq. 2) by restarted GMRES(restart)
+ * (GMRES is the default solver) with classical Gram-Schmidt
+ * applied twice (CGS2), fused dot/axpy/norm kernels, deterministic reductions.
+ * Right-preconditioned flexible GMRES when `ras` is not NULL.
+ * Convention (reading R5): u holds the initial guess on entry (pass zeros for
+ * x0 = 0) and the solution on exit; convergence when the Givens residual
+ * estimate <= rtol * ||f||_2; maxit bounds the total Arnoldi steps.
+ * f, u: nA doubles (device or host).  stats may be NULL.  Synchronises `stream`.
+ * Errors: CPM_ERR_ARG (restart < 1 or > 128, rtol <= 0), CPM_ERR_CUDA,
+ * CPM_ERR_NOMEM. Not converging within maxit is NOT an error (stats.converged = 0). */
+int cpm_solve(const cpm_band* band, double c, const double* f, double* u, double rtol, int restart,
+              int maxit, const cpm_ras* ras, cpm_solve_stats* stats, void* stream);
+
+/* ---------------------------------------------------------------- RAS preconditioner
+ * cpm_ras_setup — one-level restricted additive Schwarz, PAPER.md:87-111 with
+ * Dirichlet transmission (T_jk = identity; the default,
+ * PAPER.md:252).  Disjoint subdomains = n_sub Morton slabs of the band order
+ * (reading R8); each grown by `overlap` lattice 6-neighbour layers inside
+ * Sigma_A (reading R7).  Local solves: exactly k_inner GMRES steps from zero on
+ * A_j = R_j A R_j^T, batched over subdomains on the GPU (reading R6).
+ * c: the shift of the operator being preconditioned.
+ * Errors: CPM_ERR_ARG (n_sub < 1, overlap < 0, k_inner < 1 or > 64), CPM_ERR_CUDA. */
+int cpm_ras_setup(const cpm_band* band, int n_sub, int overlap, int k_inner, double c,
+                  void* stream, cpm_ras** out);
+/* z = sum_j R~_j^T GMRES_k(A_j, R_j r): r, z nA doubles (device or host), no aliasing. */
+int cpm_ras_apply(const cpm_ras* ras, const double* r, double* z, void* stream);
+void cpm_ras_free(cpm_ras* ras);
+
+/* ---------------------------------------------------------------- problem data
+ * cpm_eval_sph — out_i = scale * Y_l^m(cp(x_i)) on the active nodes, real
+ * orthonormal spherical harmonics without Condon-Shortley phase (reading R9);
+ * the manufactured right-hand sides of BASELINE configs 0, 1, 3.
+ * Requires a sphere band.  out: nA doubles (device or host). */
+int cpm_eval_sph(const cpm_band* band, int l, int m, double scale, double* out, void* stream);
+/* cpm_eval_torus_rhs — out_i = cos(3 th) sin(2 ph) (1 + sum_q a_q sin(k_q . cp))
+ * at cp(x_i) of a torus band (BASELINE config 2, reading R10).  coeffs: HOST
+ * array of nq rows (a, kx, ky, kz). */
+int cpm_eval_torus_rhs(const cpm_band* band, const double* coeffs, int nq, double* out,
+                       void* stream);
+
+/* ---------------------------------------------------------------- profiling
+ * When enabled, every kernel launched by the library on the caller's stream is
+ * bracketed by CUDA events; cpm_profile_read sums the device time (ms) and the
+ * launch count per kernel name since the last reset.  Names: "extend",
+ * "laplace", "mdot", "cgs_update", "cgs_final", "axpy", "other". */
+int cpm_profile_enable(int on);
+int cpm_profile_reset(void);
+int cpm_profile_read(const char* name, double* ms, int64_t* launches);
+int64_t cpm_kernel_launches(void); /* total kernels launched by the library (all names) */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CPM_H_ */

@@ -1,0 +1,330 @@
+"""Thin Python binding of the C ABI in include/cpm.h (argument marshalling only).
+
+Every function here has the name of the C entry point it calls.  Arrays may be
+torch tensors (CUDA or CPU) or numpy arrays; all must be float64, contiguous,
+of length n_active.  Device tensors are passed as device pointers on the
+current torch stream; host arrays are passed as host pointers and staged by the
+library.  There is no fallback: if libcpm.so is missing or a call fails, an
+exception is raised.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_lib", "libcpm.so")
+
+SPHERE = 1
+TORUS = 2
+
+
+class CpmError(RuntimeError):
+    pass
+
+
+class _Surface(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("param", ctypes.c_double * 4)]
+
+
+class _BandInfo(ctypes.Structure):
+    _fields_ = [
+        ("n_active", ctypes.c_int64),
+        ("n_ghost", ctypes.c_int64),
+        ("n_tiles", ctypes.c_int64),
+        ("n_runs", ctypes.c_int64),
+        ("max_box", ctypes.c_int64),
+        ("bytes_device", ctypes.c_int64),
+        ("h", ctypes.c_double),
+        ("lam", ctypes.c_double),
+        ("L", ctypes.c_double),
+        ("lattice_lo", ctypes.c_int32 * 3),
+        ("lattice_hi", ctypes.c_int32 * 3),
+        ("zero_fill", ctypes.c_int32),
+        ("rank", ctypes.c_int32),
+        ("nranks", ctypes.c_int32),
+        ("n_owned", ctypes.c_int64),
+        ("n_halo", ctypes.c_int64),
+    ]
+
+
+class _SolveStats(ctypes.Structure):
+    _fields_ = [
+        ("iterations", ctypes.c_int32),
+        ("converged", ctypes.c_int32),
+        ("cycles", ctypes.c_int32),
+        ("breakdown", ctypes.c_int32),
+        ("resid_est", ctypes.c_double),
+        ("resid_true", ctypes.c_double),
+        ("bnorm", ctypes.c_double),
+        ("seconds", ctypes.c_double),
+    ]
+
+
+_vp = ctypes.c_void_p
+_SIGS = {
+    "cpm_version": (ctypes.c_char_p, []),
+    "cpm_last_error": (ctypes.c_char_p, []),
+    "cpm_build_band": (ctypes.c_int, [ctypes.POINTER(_Surface), ctypes.c_double, ctypes.c_int,
+                                      ctypes.c_double, _vp, ctypes.POINTER(_vp)]),
+    "cpm_band_get_info": (ctypes.c_int, [_vp, ctypes.POINTER(_BandInfo)]),
+    "cpm_band_active_coords": (ctypes.c_int, [_vp, _vp]),
+    "cpm_band_ghost_coords": (ctypes.c_int, [_vp, _vp]),
+    "cpm_band_free": (None, [_vp]),
+    "cpm_apply": (ctypes.c_int, [_vp, ctypes.c_double, _vp, _vp, _vp]),
+    "cpm_solve": (ctypes.c_int, [_vp, ctypes.c_double, _vp, _vp, ctypes.c_double, ctypes.c_int,
+                                 ctypes.c_int, _vp, ctypes.POINTER(_SolveStats), _vp]),
+    "cpm_ras_setup": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                     ctypes.c_double, _vp, ctypes.POINTER(_vp)]),
+    "cpm_ras_apply": (ctypes.c_int, [_vp, _vp, _vp, _vp]),
+    "cpm_ras_free": (None, [_vp]),
+    "cpm_eval_sph": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, ctypes.c_double, _vp, _vp]),
+    "cpm_eval_torus_rhs": (ctypes.c_int, [_vp, _vp, ctypes.c_int, _vp, _vp]),
+    "cpm_profile_enable": (ctypes.c_int, [ctypes.c_int]),
+    "cpm_profile_reset": (ctypes.c_int, []),
+    "cpm_profile_read": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(ctypes.c_double),
+                                        ctypes.POINTER(ctypes.c_int64)]),
+    "cpm_kernel_launches": (ctypes.c_int64, []),
+}
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
+    """Load libcpm.so (raises if it was not built — no fallback exists)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise CpmError(f"{path} not found: build it with __graft_entry__.build() "
+                       "(python -m paper_2110_06322_b200._build)")
+    lib = ctypes.CDLL(path)
+    for name, (res, args) in _SIGS.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def exported_symbols() -> list[str]:
+    return list(_SIGS)
+
+
+def _check(rc: int, what: str):
+    if rc != 0:
+        msg = load_library().cpm_last_error().decode(errors="replace")
+        raise CpmError(f"{what} failed (code {rc}): {msg}")
+
+
+def _ptr_stream(x, n: int, writable: bool):
+    """(pointer, stream) for a float64 torch tensor / numpy array of length n."""
+    try:
+        import torch
+    except ImportError:  # pragma: no cover
+        torch = None
+    if torch is not None and isinstance(x, torch.Tensor):
+        if x.dtype != torch.float64 or not x.is_contiguous() or x.numel() != n:
+            raise CpmError(f"expected a contiguous float64 tensor of {n} elements, got "
+                           f"{x.dtype} {tuple(x.shape)}")
+        stream = torch.cuda.current_stream(x.device).cuda_stream if x.is_cuda else None
+        return x.data_ptr(), stream
+    if isinstance(x, np.ndarray):
+        if x.dtype != np.float64 or not x.flags.c_contiguous or x.size != n:
+            raise CpmError(f"expected a contiguous float64 array of {n} elements")
+        if writable and not x.flags.writeable:
+            raise CpmError("output array is read-only")
+        return x.ctypes.data, None
+    raise CpmError(f"unsupported array type {type(x)}")
+
+
+@dataclass
+class BandInfo:
+    n_active: int
+    n_ghost: int
+    n_tiles: int
+    n_runs: int
+    max_box: int
+    bytes_device: int
+    h: float
+    lam: float
+    L: float
+    zero_fill: bool
+    n_owned: int
+    n_halo: int
+    rank: int
+    nranks: int
+
+
+class Band:
+    """Owning wrapper of a cpm_band handle."""
+
+    def __init__(self, handle, surface_kind: int, params):
+        self._h = handle
+        self.surface_kind = surface_kind
+        self.params = tuple(params)
+        info = _BandInfo()
+        _check(load_library().cpm_band_get_info(self._h, ctypes.byref(info)), "cpm_band_get_info")
+        self.info = BandInfo(info.n_active, info.n_ghost, info.n_tiles, info.n_runs, info.max_box,
+                             info.bytes_device, info.h, info.lam, info.L, bool(info.zero_fill),
+                             info.n_owned, info.n_halo, info.rank, info.nranks)
+
+    @property
+    def handle(self):
+        return self._h
+
+    @property
+    def n(self) -> int:
+        return self.info.n_active
+
+    def close(self):
+        if self._h:
+            load_library().cpm_band_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def cpm_build_band(kind: str, h: float, p: int = 3, L: float = 2.0, stream=None, **params) -> Band:
+    """cpm_build_band(surface, h, p=3): the lambda-tube band of a sphere or torus."""
+    lib = load_library()
+    s = _Surface()
+    if kind == "sphere":
+        s.kind = SPHERE
+        s.param[0] = params.get("R", 1.0)
+    elif kind == "torus":
+        s.kind = TORUS
+        s.param[0] = params.get("R", 1.0)
+        s.param[1] = params.get("r", 0.4)
+    else:
+        raise CpmError(f"unknown surface {kind!r}")
+    out = _vp()
+    _check(lib.cpm_build_band(ctypes.byref(s), float(h), int(p), float(L), stream, ctypes.byref(out)),
+           "cpm_build_band")
+    return Band(out, s.kind, list(s.param))
+
+
+def cpm_band_active_coords(band: Band) -> np.ndarray:
+    out = np.empty((band.n, 3), dtype=np.int32)
+    _check(load_library().cpm_band_active_coords(band.handle, out.ctypes.data), "cpm_band_active_coords")
+    return out
+
+
+def cpm_band_ghost_coords(band: Band) -> np.ndarray:
+    out = np.empty((band.info.n_ghost, 3), dtype=np.int32)
+    _check(load_library().cpm_band_ghost_coords(band.handle, out.ctypes.data), "cpm_band_ghost_coords")
+    return out
+
+
+def cpm_apply(band: Band, c: float, u, y, stream=None):
+    """y = (c I - Delta_S^h) u."""
+    pu, su = _ptr_stream(u, band.n, False)
+    py, sy = _ptr_stream(y, band.n, True)
+    _check(load_library().cpm_apply(band.handle, float(c), pu, py, stream or su or sy), "cpm_apply")
+    return y
+
+
+@dataclass
+class SolveStats:
+    iterations: int
+    converged: bool
+    cycles: int
+    breakdown: bool
+    resid_est: float
+    resid_true: float
+    bnorm: float
+    seconds: float
+
+
+def cpm_solve(band: Band, c: float, f, u, rtol: float = 1e-10, restart: int = 30,
+              maxit: int = 100000, ras=None, stream=None) -> SolveStats:
+    """Solve (c - Delta_S^h) u = f by (F)GMRES(restart); u holds x0 on entry."""
+    pf, sf = _ptr_stream(f, band.n, False)
+    pu, su = _ptr_stream(u, band.n, True)
+    st = _SolveStats()
+    _check(load_library().cpm_solve(band.handle, float(c), pf, pu, float(rtol), int(restart), int(maxit),
+                                    ras.handle if ras is not None else None, ctypes.byref(st),
+                                    stream or sf or su), "cpm_solve")
+    return SolveStats(st.iterations, bool(st.converged), st.cycles, bool(st.breakdown), st.resid_est,
+                      st.resid_true, st.bnorm, st.seconds)
+
+
+class Ras:
+    def __init__(self, handle, band: Band):
+        self._h = handle
+        self.band = band
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self):
+        if self._h:
+            load_library().cpm_ras_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def cpm_ras_setup(band: Band, n_sub: int, overlap: int, k_inner: int, c: float, stream=None) -> Ras:
+    out = _vp()
+    _check(load_library().cpm_ras_setup(band.handle, int(n_sub), int(overlap), int(k_inner), float(c),
+                                        stream, ctypes.byref(out)), "cpm_ras_setup")
+    return Ras(out, band)
+
+
+def cpm_ras_apply(ras: Ras, r, z, stream=None):
+    pr, sr = _ptr_stream(r, ras.band.n, False)
+    pz, sz = _ptr_stream(z, ras.band.n, True)
+    _check(load_library().cpm_ras_apply(ras.handle, pr, pz, stream or sr or sz), "cpm_ras_apply")
+    return z
+
+
+def cpm_eval_sph(band: Band, l: int, m: int, scale: float, out, stream=None):
+    po, so = _ptr_stream(out, band.n, True)
+    _check(load_library().cpm_eval_sph(band.handle, int(l), int(m), float(scale), po, stream or so),
+           "cpm_eval_sph")
+    return out
+
+
+def cpm_eval_torus_rhs(band: Band, coeffs: np.ndarray, out, stream=None):
+    co = np.ascontiguousarray(coeffs, dtype=np.float64)
+    po, so = _ptr_stream(out, band.n, True)
+    _check(load_library().cpm_eval_torus_rhs(band.handle, co.ctypes.data, int(co.shape[0]), po,
+                                             stream or so), "cpm_eval_torus_rhs")
+    return out
+
+
+def cpm_profile_enable(on: bool = True):
+    _check(load_library().cpm_profile_enable(1 if on else 0), "cpm_profile_enable")
+
+
+def cpm_profile_reset():
+    _check(load_library().cpm_profile_reset(), "cpm_profile_reset")
+
+
+def cpm_profile_read(name: str):
+    ms = ctypes.c_double()
+    n = ctypes.c_int64()
+    _check(load_library().cpm_profile_read(name.encode(), ctypes.byref(ms), ctypes.byref(n)),
+           "cpm_profile_read")
+    return ms.value, n.value
+
+
+def cpm_kernel_launches() -> int:
+    return int(load_library().cpm_kernel_launches())
+
+
+def cpm_version() -> str:
+    return load_library().cpm_version().decode()

@@ -1,0 +1,629 @@
+// build.cu — band construction on the GPU (north_star item 1).
+//
+// Pipeline (all on the caller's stream):
+//   B1  brick candidates: every 8^3 brick of the surface's padded box whose
+//       centre lies within lambda + h + half-diagonal of the surface (the
+//       distance function is 1-Lipschitz, so no band or ghost node is missed)
+//   B2  radix-sort candidate bricks by Morton code (band order, reading R8)
+//   B3  classify the 512 nodes of each candidate: Sigma_A (dist <= lambda,
+//       inside [-L, L]^3) and Sigma_G (not in Sigma_A, a 6-neighbour in it);
+//       per-brick 512-bit masks and counts
+//   B4  scans -> tile slots, active/eval/ghost starts
+//   B5  per node: closest point, stencil base floor(cp/h) - 1, offset
+//       t = cp/h - floor(cp/h) (reading R2); coordinates for the caller
+//   B6  dense brick map (bucketed node -> lattice index map), per-tile stencil
+//       box and face neighbours, per-node box offsets, stencil coverage check
+//   B7  stencil-box fill runs (consecutive band-order sources -> box rows)
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <climits>
+#include <memory>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "geom.cuh"
+#include "internal.cuh"
+
+namespace cpm {
+namespace {
+
+struct BuildParams {
+  Surface s;
+  double h, lam, slack;
+  int M;
+  int blo[3], bdim[3];  // brick box
+};
+
+// ------------------------------------------------------------------ B1
+__global__ void k_brick_candidates(BuildParams P, uint64_t* keys, int* count) {
+  int64_t n = (int64_t)P.bdim[0] * P.bdim[1] * P.bdim[2];
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    int bx = (int)(t % P.bdim[0]) + P.blo[0];
+    int by = (int)((t / P.bdim[0]) % P.bdim[1]) + P.blo[1];
+    int bz = (int)(t / ((int64_t)P.bdim[0] * P.bdim[1])) + P.blo[2];
+    double cx = (bx * 8 + 3.5) * P.h, cy = (by * 8 + 3.5) * P.h, cz = (bz * 8 + 3.5) * P.h;
+    double d = surface_dist(P.s, cx, cy, cz);
+    // conservative: half-diagonal 3.5*sqrt(3)*h, plus one h for ghosts
+    if (!(d <= P.lam + P.h + 3.5 * 1.7320508075688772 * P.h + P.slack)) continue;
+    int slot = atomicAdd(count, 1);
+    keys[slot] = brick_morton(bx, by, bz);
+  }
+}
+
+__device__ inline bool in_domain(int i, int j, int k, int M) {
+  return i >= -M && i <= M && j >= -M && j <= M && k >= -M && k <= M;
+}
+
+__device__ inline bool is_active(const BuildParams& P, int i, int j, int k) {
+  if (!in_domain(i, j, k, P.M)) return false;
+  double d = surface_dist(P.s, lat(i, P.h), lat(j, P.h), lat(k, P.h));
+  return d <= P.lam;
+}
+
+// ------------------------------------------------------------------ B3
+// One CTA of 512 threads per candidate brick; thread = cell lx + 8 ly + 64 lz.
+__global__ void __launch_bounds__(512) k_classify(BuildParams P, const uint64_t* keys,
+                                                  uint32_t* amask, uint32_t* gmask, int* na,
+                                                  int* ng, int* ne) {
+  int b = blockIdx.x;
+  int bx, by, bz;
+  morton_brick(keys[b], &bx, &by, &bz);
+  int c = threadIdx.x;
+  int i = bx * 8 + (c & 7), j = by * 8 + ((c >> 3) & 7), k = bz * 8 + (c >> 6);
+  bool a = is_active(P, i, j, k);
+  bool g = false;
+  if (!a) {
+    g = is_active(P, i + 1, j, k) || is_active(P, i - 1, j, k) || is_active(P, i, j + 1, k) ||
+        is_active(P, i, j - 1, k) || is_active(P, i, j, k + 1) || is_active(P, i, j, k - 1);
+  }
+  uint32_t am = __ballot_sync(0xffffffffu, a);
+  uint32_t gm = __ballot_sync(0xffffffffu, g);
+  __shared__ int sa[16], sg[16];
+  int w = c >> 5;
+  if ((c & 31) == 0) {
+    amask[(size_t)b * 16 + w] = am;
+    gmask[(size_t)b * 16 + w] = gm;
+    sa[w] = __popc(am);
+    sg[w] = __popc(gm);
+  }
+  __syncthreads();
+  if (c == 0) {
+    int ta = 0, tg = 0;
+    for (int q = 0; q < 16; ++q) {
+      ta += sa[q];
+      tg += sg[q];
+    }
+    na[b] = ta;
+    ng[b] = tg;
+    ne[b] = ta + tg;
+  }
+}
+
+__device__ inline int mask_rank(const uint32_t* m16, int cell) {
+  int w = cell >> 5, r = 0;
+  for (int q = 0; q < w; ++q) r += __popc(m16[q]);
+  return r + __popc(m16[w] & ((1u << (cell & 31)) - 1u));
+}
+__device__ inline bool mask_has(const uint32_t* m16, int cell) {
+  return (m16[cell >> 5] >> (cell & 31)) & 1u;
+}
+
+// ------------------------------------------------------------------ B4 helpers
+__global__ void k_compact_tiles(int nb, const int* ne, const int* tslot, const int* na,
+                                const int* ng, const int* astart, const int* gstart,
+                                const int* estart, const uint64_t* keys, const uint32_t* amask,
+                                const uint32_t* gmask, TileHdr* tiles, uint32_t* tam,
+                                uint32_t* tgm, int* tgstart) {
+  int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= nb || ne[b] == 0) return;
+  int t = tslot[b];
+  TileHdr T;
+  memset(&T, 0, sizeof(T));
+  T.e0 = estart[b];
+  T.e1 = estart[b] + ne[b];
+  T.a0 = astart[b];
+  T.a1 = astart[b] + na[b];
+  morton_brick(keys[b], &T.bx, &T.by, &T.bz);
+  for (int q = 0; q < 6; ++q) T.nbr[q] = -1;
+  tiles[t] = T;
+  tgstart[t] = gstart[b];
+  for (int q = 0; q < 16; ++q) {
+    tam[(size_t)t * 16 + q] = amask[(size_t)b * 16 + q];
+    tgm[(size_t)t * 16 + q] = gmask[(size_t)b * 16 + q];
+  }
+}
+
+// ------------------------------------------------------------------ B5
+// One CTA (512 threads) per tile.  Eval order inside a tile: Sigma_A cells in
+// lexicographic order, then Sigma_G cells.
+__global__ void __launch_bounds__(512) k_node_data(BuildParams P, const TileHdr* tiles,
+                                                   const uint32_t* tam, const uint32_t* tgm,
+                                                   const int* tgstart, int32_t* aijk,
+                                                   int32_t* gijk, uint16_t* acell, double* tx,
+                                                   double* ty, double* tz, int32_t* ebase,
+                                                   uint16_t* ecell, int* err) {
+  int t = blockIdx.x;
+  __shared__ uint32_t am[16], gm[16];
+  if (threadIdx.x < 16) {
+    am[threadIdx.x] = tam[(size_t)t * 16 + threadIdx.x];
+    gm[threadIdx.x] = tgm[(size_t)t * 16 + threadIdx.x];
+  }
+  __syncthreads();
+  const TileHdr T = tiles[t];
+  int c = threadIdx.x;
+  bool a = mask_has(am, c), g = mask_has(gm, c);
+  if (!a && !g) return;
+  int i = T.bx * 8 + (c & 7), j = T.by * 8 + ((c >> 3) & 7), k = T.bz * 8 + (c >> 6);
+  int e;
+  if (a) {
+    int ra = mask_rank(am, c);
+    int ai = T.a0 + ra;
+    aijk[3 * (size_t)ai + 0] = i;
+    aijk[3 * (size_t)ai + 1] = j;
+    aijk[3 * (size_t)ai + 2] = k;
+    acell[ai] = (uint16_t)c;
+    e = T.e0 + ra;
+  } else {
+    int rg = mask_rank(gm, c);
+    int gi = tgstart[t] + rg;
+    gijk[3 * (size_t)gi + 0] = i;
+    gijk[3 * (size_t)gi + 1] = j;
+    gijk[3 * (size_t)gi + 2] = k;
+    e = T.e0 + (T.a1 - T.a0) + rg;
+  }
+  double cx, cy, cz, d;
+  bool ok = closest_point(P.s, lat(i, P.h), lat(j, P.h), lat(k, P.h), &cx, &cy, &cz, &d);
+  if (!ok || !isfinite(cx) || !isfinite(cy) || !isfinite(cz)) {
+    atomicOr(err, 1);
+    cx = cy = cz = 0.0;
+  }
+  // s = cp/h, base = floor(s) - 1, t = s - floor(s)   (reading R2)
+  double sx = RN_DIV(cx, P.h), sy = RN_DIV(cy, P.h), sz = RN_DIV(cz, P.h);
+  double fx = floor(sx), fy = floor(sy), fz = floor(sz);
+  tx[e] = RN_SUB(sx, fx);
+  ty[e] = RN_SUB(sy, fy);
+  tz[e] = RN_SUB(sz, fz);
+  ebase[3 * (size_t)e + 0] = (int)fx - 1;
+  ebase[3 * (size_t)e + 1] = (int)fy - 1;
+  ebase[3 * (size_t)e + 2] = (int)fz - 1;
+  ecell[e] = (uint16_t)c;
+}
+
+// ------------------------------------------------------------------ B6
+__global__ void k_brick_map(int nT, const TileHdr* tiles, const int* blo, const int* bdim,
+                            int* bmap) {
+  int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nT) return;
+  int x = tiles[t].bx - blo[0], y = tiles[t].by - blo[1], z = tiles[t].bz - blo[2];
+  bmap[((size_t)z * bdim[1] + y) * bdim[0] + x] = t;
+}
+
+__device__ inline int bmap_get(const int* bmap, const int* blo, const int* bdim, int bx, int by,
+                               int bz) {
+  int x = bx - blo[0], y = by - blo[1], z = bz - blo[2];
+  if (x < 0 || y < 0 || z < 0 || x >= bdim[0] || y >= bdim[1] || z >= bdim[2]) return -1;
+  return bmap[((size_t)z * bdim[1] + y) * bdim[0] + x];
+}
+
+// Per tile: stencil box = bounding box of the eval nodes' 4^3 stencils.
+__global__ void __launch_bounds__(256) k_tile_box(int nT, TileHdr* tiles, const int32_t* ebase,
+                                                  const int* bmap, const int* blo,
+                                                  const int* bdim, int* err, int* maxbox) {
+  int t = blockIdx.x;
+  TileHdr T = tiles[t];
+  int lo[3] = {INT_MAX, INT_MAX, INT_MAX}, hi[3] = {INT_MIN, INT_MIN, INT_MIN};
+  for (int e = T.e0 + threadIdx.x; e < T.e1; e += blockDim.x) {
+    for (int q = 0; q < 3; ++q) {
+      int v = ebase[3 * (size_t)e + q];
+      lo[q] = min(lo[q], v);
+      hi[q] = max(hi[q], v);
+    }
+  }
+  using BR = cub::BlockReduce<int, 256>;
+  __shared__ typename BR::TempStorage tmp;
+  __shared__ int res[6];
+  for (int q = 0; q < 3; ++q) {
+    int a = BR(tmp).Reduce(lo[q], cub::Min());
+    __syncthreads();
+    int b = BR(tmp).Reduce(hi[q], cub::Max());
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      res[q] = a;
+      res[3 + q] = b;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    T.ox = res[0];
+    T.oy = res[1];
+    T.oz = res[2];
+    T.sx = res[3] - res[0] + 4;
+    T.sy = res[4] - res[1] + 4;
+    T.sz = res[5] - res[2] + 4;
+    int cells = T.sx * T.sy * T.sz;
+    if (T.sx > kMaxBoxEdge || T.sy > kMaxBoxEdge || T.sz > kMaxBoxEdge || cells > kMaxBoxCells)
+      atomicOr(err, 2);
+    atomicMax(maxbox, cells);
+    T.nbr[0] = bmap_get(bmap, blo, bdim, T.bx + 1, T.by, T.bz);
+    T.nbr[1] = bmap_get(bmap, blo, bdim, T.bx - 1, T.by, T.bz);
+    T.nbr[2] = bmap_get(bmap, blo, bdim, T.bx, T.by + 1, T.bz);
+    T.nbr[3] = bmap_get(bmap, blo, bdim, T.bx, T.by - 1, T.bz);
+    T.nbr[4] = bmap_get(bmap, blo, bdim, T.bx, T.by, T.bz + 1);
+    T.nbr[5] = bmap_get(bmap, blo, bdim, T.bx, T.by, T.bz - 1);
+    tiles[t] = T;
+  }
+}
+
+// Per eval node: box offset of its stencil base; stencil coverage check (every
+// stencil cell must be a source node, i.e. in Sigma_A: StencilEscape otherwise).
+__global__ void k_eoff(int nT, const TileHdr* tiles, const int32_t* ebase, const uint16_t* ecell,
+                       const uint32_t* tam, const int* bmap, const int* blo, const int* bdim,
+                       uint32_t* eoff, int* err) {
+  int t = blockIdx.x;
+  const TileHdr T = tiles[t];
+  for (int e = T.e0 + threadIdx.x; e < T.e1; e += blockDim.x) {
+    int b0 = ebase[3 * (size_t)e], b1 = ebase[3 * (size_t)e + 1], b2 = ebase[3 * (size_t)e + 2];
+    uint32_t off = (uint32_t)((b0 - T.ox) + T.sx * ((b1 - T.oy) + T.sy * (b2 - T.oz)));
+    eoff[e] = off | ((uint32_t)ecell[e] << 16);
+    bool ok = true;
+    for (int cz = 0; cz < 4 && ok; ++cz)
+      for (int cy = 0; cy < 4 && ok; ++cy)
+        for (int cx = 0; cx < 4 && ok; ++cx) {
+          int i = b0 + cx, j = b1 + cy, k = b2 + cz;
+          int s = bmap_get(bmap, blo, bdim, brick_of(i), brick_of(j), brick_of(k));
+          if (s < 0) {
+            ok = false;
+            break;
+          }
+          int cell = local_of(i) + 8 * local_of(j) + 64 * local_of(k);
+          if (!mask_has(tam + (size_t)s * 16, cell)) ok = false;
+        }
+    if (!ok) atomicOr(err, 4);
+  }
+}
+
+// ------------------------------------------------------------------ B7
+// Thread per (tile, box row).  Walk the row's x range brick by brick; maximal
+// segments of consecutive Sigma_A cells inside one brick row are consecutive in
+// band order and become one run (source = band-order index of the first cell).
+__global__ void k_rows_per_tile(int nT, const TileHdr* tiles, int64_t* nrows) {
+  int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < nT) nrows[t] = (int64_t)tiles[t].sy * tiles[t].sz;
+  if (t == 0) nrows[nT] = 0;
+}
+
+template <bool WRITE>
+__global__ void k_runs(const TileHdr* tiles, const uint32_t* tam, const int* bmap, const int* blo,
+                       const int* bdim, const int64_t* rowbase, int64_t* rowcnt,
+                       const int64_t* runstart, uint64_t* runs) {
+  int t = blockIdx.x;
+  const TileHdr T = tiles[t];
+  int nrows = T.sy * T.sz;
+  for (int r = threadIdx.x; r < nrows; r += blockDim.x) {
+    int y = T.oy + r % T.sy, z = T.oz + r / T.sy;
+    int by = brick_of(y), bz = brick_of(z), ly = local_of(y), lz = local_of(z);
+    int64_t gi = rowbase[t] + r;
+    int64_t out = WRITE ? runstart[gi] : 0;
+    int64_t n = 0;
+    int x = T.ox, xe = T.ox + T.sx;
+    while (x < xe) {
+      int bx = brick_of(x);
+      int xend = min(xe, bx * 8 + 8);
+      int s = bmap_get(bmap, blo, bdim, bx, by, bz);
+      if (s >= 0) {
+        const uint32_t* m = tam + (size_t)s * 16;
+        int q = local_of(x), lxe = xend - bx * 8;
+        while (q < lxe) {
+          if (!mask_has(m, q + 8 * ly + 64 * lz)) {
+            ++q;
+            continue;
+          }
+          int q0 = q;
+          while (q < lxe && mask_has(m, q + 8 * ly + 64 * lz)) ++q;
+          if (WRITE) {
+            uint32_t src = (uint32_t)(tiles[s].a0 + mask_rank(m, q0 + 8 * ly + 64 * lz));
+            uint32_t dst =
+                (uint32_t)((bx * 8 + q0 - T.ox) + T.sx * ((y - T.oy) + T.sy * (z - T.oz)));
+            runs[out + n] = pack_run(src, dst, (uint32_t)(q - q0));
+          }
+          ++n;
+        }
+      }
+      x = xend;
+    }
+    if (!WRITE) rowcnt[gi] = n;
+  }
+}
+
+__global__ void k_set_run_ranges(int nT, TileHdr* tiles, const int64_t* rowbase,
+                                 const int64_t* runstart) {
+  int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nT) return;
+  tiles[t].r0 = (int32_t)runstart[rowbase[t]];
+  tiles[t].r1 = (int32_t)runstart[rowbase[t + 1]];
+}
+
+__global__ void k_flags(int nb, const int* ne, int* flag) {
+  int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b < nb) flag[b] = ne[b] > 0 ? 1 : 0;
+  if (b == 0) flag[nb] = 0;
+}
+
+// ------------------------------------------------------------------ host helpers
+struct DevBuf {
+  void* p = nullptr;
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  template <class T>
+  T* as() {
+    return (T*)p;
+  }
+};
+
+template <class T>
+int dalloc(DevBuf& b, size_t n, const char* what) {
+  cudaError_t e = cudaMalloc(&b.p, std::max<size_t>(n, 1) * sizeof(T));
+  if (e != cudaSuccess) return fail(CPM_ERR_NOMEM, std::string("cudaMalloc failed for ") + what);
+  return CPM_OK;
+}
+
+template <class T>
+int dalloc_owned(T** p, size_t n, int64_t* bytes, const char* what) {
+  cudaError_t e = cudaMalloc((void**)p, std::max<size_t>(n, 1) * sizeof(T));
+  if (e != cudaSuccess) return fail(CPM_ERR_NOMEM, std::string("cudaMalloc failed for ") + what);
+  *bytes += (int64_t)(std::max<size_t>(n, 1) * sizeof(T));
+  return CPM_OK;
+}
+
+template <class T>
+int exclusive_sum(const T* in, T* out, int64_t n, cudaStream_t s) {
+  size_t tmp = 0;
+  CPM_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, in, out, n, s));
+  DevBuf tb;
+  CPM_TRY(dalloc<char>(tb, tmp, "scan temp"));
+  CPM_CUDA(cub::DeviceScan::ExclusiveSum(tb.p, tmp, in, out, n, s));
+  return CPM_OK;
+}
+
+template <class T>
+int read_back(const T* dptr, T* hval, cudaStream_t s) {
+  CPM_CUDA(cudaMemcpyAsync(hval, dptr, sizeof(T), cudaMemcpyDeviceToHost, s));
+  CPM_CUDA(cudaStreamSynchronize(s));
+  return CPM_OK;
+}
+
+inline int grid_for(int64_t n, int bs) { return (int)std::max<int64_t>(1, std::min<int64_t>((n + bs - 1) / bs, 1 << 30)); }
+
+}  // namespace
+
+void free_workspace(Workspace* w);
+
+void free_band(cpm_band* b) {
+  if (!b) return;
+  if (b->ws) free_workspace(b->ws);
+  void* ptrs[] = {b->tiles, b->tx,  b->ty,   b->tz, b->eoff, b->acell, b->aijk,
+                  b->gijk,  b->runs, b->vb, b->dstage0, b->dstage1};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  delete b;
+}
+
+int build_band(const cpm_surface* surf, double h, int p, double L, cudaStream_t s,
+               cpm_band** out) {
+  if (!surf || !out) return fail(CPM_ERR_ARG, "cpm_build_band: null argument");
+  *out = nullptr;
+  if (p != 3) return fail(CPM_ERR_ARG, "cpm_build_band: only p = 3 (tricubic) is implemented");
+  if (!(h > 0.0) || !(L > 0.0)) return fail(CPM_ERR_ARG, "cpm_build_band: h and L must be > 0");
+  if (surf->kind != CPM_SURF_SPHERE && surf->kind != CPM_SURF_TORUS)
+    return fail(CPM_ERR_ARG, "cpm_build_band: unknown surface kind");
+  if (surf->kind == CPM_SURF_SPHERE && !(surf->param[0] > 0.0))
+    return fail(CPM_ERR_ARG, "cpm_build_band: sphere radius must be > 0");
+  if (surf->kind == CPM_SURF_TORUS && !(surf->param[0] > surf->param[1] && surf->param[1] > 0.0))
+    return fail(CPM_ERR_ARG, "cpm_build_band: torus needs R > r > 0");
+
+  BuildParams P;
+  P.s.kind = surf->kind;
+  for (int q = 0; q < 4; ++q) P.s.p[q] = surf->param[q];
+  P.h = h;
+  P.lam = sqrt(17.0) * h;  // reading R1
+  P.M = (int)llround(L / h);
+  P.slack = 1e-9 * h;
+  if (P.M > (1 << 18)) return fail(CPM_ERR_LIMIT, "cpm_build_band: L/h too large (> 2^18)");
+  double ex, ez;
+  if (surf->kind == CPM_SURF_SPHERE) {
+    ex = ez = surf->param[0] + P.lam + 2 * h;
+  } else {
+    ex = surf->param[0] + surf->param[1] + P.lam + 2 * h;
+    ez = surf->param[1] + P.lam + 2 * h;
+  }
+  int ilo[3], ihi[3];
+  double e3[3] = {ex, ex, ez};
+  for (int q = 0; q < 3; ++q) {
+    ilo[q] = std::max(-P.M - 1, (int)floor(-e3[q] / h) - 1);
+    ihi[q] = std::min(P.M + 1, (int)ceil(e3[q] / h) + 1);
+    P.blo[q] = brick_of(ilo[q]);
+    P.bdim[q] = brick_of(ihi[q]) - P.blo[q] + 1;
+  }
+  int64_t nbox = (int64_t)P.bdim[0] * P.bdim[1] * P.bdim[2];
+
+  // B1 candidates
+  DevBuf keys, cnt;
+  CPM_TRY(dalloc<uint64_t>(keys, nbox, "brick keys"));
+  CPM_TRY(dalloc<int>(cnt, 1, "count"));
+  CPM_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(int), s));
+  k_brick_candidates<<<grid_for(nbox, 256), 256, 0, s>>>(P, keys.as<uint64_t>(), cnt.as<int>());
+  count_launch();
+  CPM_CUDA(cudaGetLastError());
+  int nb = 0;
+  CPM_TRY(read_back(cnt.as<int>(), &nb, s));
+  if (nb == 0) return fail(CPM_ERR_GEOM, "cpm_build_band: empty band (surface outside the box?)");
+
+  // B2 sort by Morton code
+  DevBuf keys2;
+  CPM_TRY(dalloc<uint64_t>(keys2, nb, "sorted keys"));
+  {
+    size_t tmp = 0;
+    CPM_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp, keys.as<uint64_t>(), keys2.as<uint64_t>(),
+                                            nb, 0, 51, s));
+    DevBuf tb;
+    CPM_TRY(dalloc<char>(tb, tmp, "sort temp"));
+    CPM_CUDA(cub::DeviceRadixSort::SortKeys(tb.p, tmp, keys.as<uint64_t>(), keys2.as<uint64_t>(),
+                                            nb, 0, 51, s));
+  }
+
+  // B3 classify
+  DevBuf amask, gmask, na, ng, ne;
+  CPM_TRY(dalloc<uint32_t>(amask, (size_t)nb * 16, "amask"));
+  CPM_TRY(dalloc<uint32_t>(gmask, (size_t)nb * 16, "gmask"));
+  CPM_TRY(dalloc<int>(na, nb + 1, "na"));
+  CPM_TRY(dalloc<int>(ng, nb + 1, "ng"));
+  CPM_TRY(dalloc<int>(ne, nb + 1, "ne"));
+  CPM_CUDA(cudaMemsetAsync(na.p, 0, (nb + 1) * sizeof(int), s));
+  CPM_CUDA(cudaMemsetAsync(ng.p, 0, (nb + 1) * sizeof(int), s));
+  CPM_CUDA(cudaMemsetAsync(ne.p, 0, (nb + 1) * sizeof(int), s));
+  k_classify<<<nb, 512, 0, s>>>(P, keys2.as<uint64_t>(), amask.as<uint32_t>(), gmask.as<uint32_t>(),
+                                na.as<int>(), ng.as<int>(), ne.as<int>());
+  count_launch();
+  CPM_CUDA(cudaGetLastError());
+
+  // B4 scans
+  DevBuf astart, gstart, estart, flag, tslot;
+  CPM_TRY(dalloc<int>(astart, nb + 1, "astart"));
+  CPM_TRY(dalloc<int>(gstart, nb + 1, "gstart"));
+  CPM_TRY(dalloc<int>(estart, nb + 1, "estart"));
+  CPM_TRY(dalloc<int>(flag, nb + 1, "flag"));
+  CPM_TRY(dalloc<int>(tslot, nb + 1, "tslot"));
+  CPM_TRY(exclusive_sum(na.as<int>(), astart.as<int>(), nb + 1, s));
+  CPM_TRY(exclusive_sum(ng.as<int>(), gstart.as<int>(), nb + 1, s));
+  CPM_TRY(exclusive_sum(ne.as<int>(), estart.as<int>(), nb + 1, s));
+  k_flags<<<grid_for(nb, 256), 256, 0, s>>>(nb, ne.as<int>(), flag.as<int>());
+  count_launch();
+  CPM_TRY(exclusive_sum(flag.as<int>(), tslot.as<int>(), nb + 1, s));
+  int totA = 0, totG = 0, totE = 0, totT = 0;
+  CPM_TRY(read_back(astart.as<int>() + nb, &totA, s));
+  CPM_TRY(read_back(gstart.as<int>() + nb, &totG, s));
+  CPM_TRY(read_back(estart.as<int>() + nb, &totE, s));
+  CPM_TRY(read_back(tslot.as<int>() + nb, &totT, s));
+  if (totA == 0) return fail(CPM_ERR_GEOM, "cpm_build_band: no active nodes");
+
+  cpm_band* B = new cpm_band();
+  std::unique_ptr<cpm_band, void (*)(cpm_band*)> guard(B, free_band);
+  B->surf = P.s;
+  B->h = h;
+  B->lam = P.lam;
+  B->L = L;
+  B->M = P.M;
+  B->nA = totA;
+  B->nG = totG;
+  B->nE = totE;
+  B->nT = totT;
+  B->nOwned = totA;
+  for (int q = 0; q < 3; ++q) {
+    B->ilo[q] = ilo[q];
+    B->ihi[q] = ihi[q];
+  }
+  DevBuf tam, tgm, tgstart;
+  CPM_TRY(dalloc_owned(&B->tiles, totT, &B->bytes, "tiles"));
+  CPM_TRY(dalloc<uint32_t>(tam, (size_t)totT * 16, "tile amask"));
+  CPM_TRY(dalloc<uint32_t>(tgm, (size_t)totT * 16, "tile gmask"));
+  CPM_TRY(dalloc<int>(tgstart, totT, "tile gstart"));
+  k_compact_tiles<<<grid_for(nb, 256), 256, 0, s>>>(
+      nb, ne.as<int>(), tslot.as<int>(), na.as<int>(), ng.as<int>(), astart.as<int>(),
+      gstart.as<int>(), estart.as<int>(), keys2.as<uint64_t>(), amask.as<uint32_t>(),
+      gmask.as<uint32_t>(), B->tiles, tam.as<uint32_t>(), tgm.as<uint32_t>(), tgstart.as<int>());
+  count_launch();
+  CPM_CUDA(cudaGetLastError());
+
+  // B5 per-node data
+  DevBuf ebase, ecell, err;
+  CPM_TRY(dalloc_owned(&B->aijk, 3 * (size_t)totA, &B->bytes, "aijk"));
+  CPM_TRY(dalloc_owned(&B->gijk, 3 * (size_t)std::max(totG, 1), &B->bytes, "gijk"));
+  CPM_TRY(dalloc_owned(&B->acell, totA, &B->bytes, "acell"));
+  CPM_TRY(dalloc_owned(&B->tx, totE, &B->bytes, "tx"));
+  CPM_TRY(dalloc_owned(&B->ty, totE, &B->bytes, "ty"));
+  CPM_TRY(dalloc_owned(&B->tz, totE, &B->bytes, "tz"));
+  CPM_TRY(dalloc_owned(&B->eoff, totE, &B->bytes, "eoff"));
+  CPM_TRY(dalloc<int32_t>(ebase, 3 * (size_t)totE, "ebase"));
+  CPM_TRY(dalloc<uint16_t>(ecell, totE, "ecell"));
+  CPM_TRY(dalloc<int>(err, 2, "err"));
+  CPM_CUDA(cudaMemsetAsync(err.p, 0, 2 * sizeof(int), s));
+  k_node_data<<<totT, 512, 0, s>>>(P, B->tiles, tam.as<uint32_t>(), tgm.as<uint32_t>(),
+                                   tgstart.as<int>(), B->aijk, B->gijk, B->acell, B->tx, B->ty,
+                                   B->tz, ebase.as<int32_t>(), ecell.as<uint16_t>(), err.as<int>());
+  count_launch();
+  CPM_CUDA(cudaGetLastError());
+
+  // B6 brick map, boxes, offsets, coverage
+  DevBuf bmap, dblo, dbdim;
+  CPM_TRY(dalloc<int>(bmap, nbox, "brick map"));
+  CPM_TRY(dalloc<int>(dblo, 3, "blo"));
+  CPM_TRY(dalloc<int>(dbdim, 3, "bdim"));
+  CPM_CUDA(cudaMemcpyAsync(dblo.p, P.blo, 3 * sizeof(int), cudaMemcpyHostToDevice, s));
+  CPM_CUDA(cudaMemcpyAsync(dbdim.p, P.bdim, 3 * sizeof(int), cudaMemcpyHostToDevice, s));
+  CPM_CUDA(cudaMemsetAsync(bmap.p, 0xff, nbox * sizeof(int), s));
+  k_brick_map<<<grid_for(totT, 256), 256, 0, s>>>(totT, B->tiles, dblo.as<int>(), dbdim.as<int>(),
+                                                   bmap.as<int>());
+  count_launch();
+  k_tile_box<<<totT, 256, 0, s>>>(totT, B->tiles, ebase.as<int32_t>(), bmap.as<int>(),
+                                  dblo.as<int>(), dbdim.as<int>(), err.as<int>(),
+                                  err.as<int>() + 1);
+  count_launch();
+  k_eoff<<<totT, 128, 0, s>>>(totT, B->tiles, ebase.as<int32_t>(), ecell.as<uint16_t>(),
+                              tam.as<uint32_t>(), bmap.as<int>(), dblo.as<int>(), dbdim.as<int>(),
+                              B->eoff, err.as<int>());
+  count_launch();
+  CPM_CUDA(cudaGetLastError());
+  int herr[2] = {0, 0};
+  CPM_CUDA(cudaMemcpyAsync(herr, err.p, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
+  CPM_CUDA(cudaStreamSynchronize(s));
+  if (herr[0] & 1)
+    return fail(CPM_ERR_GEOM,
+                "cpm_build_band: closest point undefined at a band/ghost node (lambda + h exceeds "
+                "the surface's reach, PAPER.md:62)");
+  if (herr[0] & 2) return fail(CPM_ERR_LIMIT, "cpm_build_band: a tile's stencil box exceeds the limit");
+  if (herr[0] & 4)
+    return fail(CPM_ERR_GEOM, "cpm_build_band: StencilEscape — an interpolation stencil leaves Sigma_A");
+  B->maxBox = herr[1];
+
+  // B7 fill runs
+  DevBuf nrows, rowbase, rowcnt, runstart;
+  CPM_TRY(dalloc<int64_t>(nrows, totT + 1, "nrows"));
+  CPM_TRY(dalloc<int64_t>(rowbase, totT + 1, "rowbase"));
+  k_rows_per_tile<<<grid_for(totT + 1, 256), 256, 0, s>>>(totT, B->tiles, nrows.as<int64_t>());
+  count_launch();
+  CPM_TRY(exclusive_sum(nrows.as<int64_t>(), rowbase.as<int64_t>(), totT + 1, s));
+  int64_t totRows = 0;
+  CPM_TRY(read_back(rowbase.as<int64_t>() + totT, &totRows, s));
+  CPM_TRY(dalloc<int64_t>(rowcnt, totRows + 1, "rowcnt"));
+  CPM_TRY(dalloc<int64_t>(runstart, totRows + 1, "runstart"));
+  CPM_CUDA(cudaMemsetAsync(rowcnt.p, 0, (totRows + 1) * sizeof(int64_t), s));
+  k_runs<false><<<totT, 128, 0, s>>>(B->tiles, tam.as<uint32_t>(), bmap.as<int>(), dblo.as<int>(),
+                                     dbdim.as<int>(), rowbase.as<int64_t>(), rowcnt.as<int64_t>(),
+                                     nullptr, nullptr);
+  count_launch();
+  CPM_TRY(exclusive_sum(rowcnt.as<int64_t>(), runstart.as<int64_t>(), totRows + 1, s));
+  int64_t totRuns = 0;
+  CPM_TRY(read_back(runstart.as<int64_t>() + totRows, &totRuns, s));
+  if (totRuns >= (int64_t)INT32_MAX) return fail(CPM_ERR_LIMIT, "cpm_build_band: too many runs");
+  CPM_TRY(dalloc_owned(&B->runs, totRuns, &B->bytes, "runs"));
+  k_runs<true><<<totT, 128, 0, s>>>(B->tiles, tam.as<uint32_t>(), bmap.as<int>(), dblo.as<int>(),
+                                    dbdim.as<int>(), rowbase.as<int64_t>(), rowcnt.as<int64_t>(),
+                                    runstart.as<int64_t>(), B->runs);
+  count_launch();
+  k_set_run_ranges<<<grid_for(totT, 256), 256, 0, s>>>(totT, B->tiles, rowbase.as<int64_t>(),
+                                                        runstart.as<int64_t>());
+  count_launch();
+  CPM_CUDA(cudaGetLastError());
+  B->nRuns = totRuns;
+
+  CPM_TRY(dalloc_owned(&B->vb, (size_t)totT * kBrickCells, &B->bytes, "vb"));
+  CPM_CUDA(cudaStreamSynchronize(s));
+  *out = guard.release();
+  return CPM_OK;
+}
+
+}  // namespace cpm

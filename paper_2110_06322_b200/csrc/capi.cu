@@ -1,0 +1,241 @@
+// capi.cu — the extern "C" boundary (include/cpm.h): argument checks, host-pointer
+// staging, error state, profiling.  Every compute step runs in the kernels of
+// build.cu / apply.cu / krylov.cu / ras.cu / problems.cu.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "internal.cuh"
+#include "krylov.cuh"
+
+namespace cpm {
+
+// ------------------------------------------------------------------ errors
+static thread_local std::string g_err;
+
+void set_error(const std::string& msg) { g_err = msg; }
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+int cuda_fail(cudaError_t e, const char* what, const char* file, int line) {
+  g_err = std::string("CUDA error ") + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) +
+          ") in " + what + " at " + file + ":" + std::to_string(line);
+  return CPM_ERR_CUDA;
+}
+
+// ------------------------------------------------------------------ profiling
+namespace {
+std::atomic<int64_t> g_launches{0};
+std::mutex g_prof_mu;
+bool g_prof_on = false;
+struct Pending {
+  int id;
+  cudaEvent_t a, b;
+};
+std::vector<Pending> g_pending;
+std::vector<cudaEvent_t> g_pool;
+double g_ms[K_COUNT] = {0};
+int64_t g_cnt[K_COUNT] = {0};
+const char* g_names[K_COUNT] = {"extend", "laplace", "mdot", "cgs_update", "cgs_final", "axpy", "other"};
+
+cudaEvent_t take_event() {
+  if (!g_pool.empty()) {
+    cudaEvent_t e = g_pool.back();
+    g_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+void drain_pending() {
+  for (auto& p : g_pending) {
+    cudaEventSynchronize(p.b);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, p.a, p.b);
+    g_ms[p.id] += ms;
+    g_cnt[p.id] += 1;
+    g_pool.push_back(p.a);
+    g_pool.push_back(p.b);
+  }
+  g_pending.clear();
+}
+}  // namespace
+
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+ProfScope::ProfScope(KernelId id_, cudaStream_t s_) : id(id_), s(s_) {
+  if (!g_prof_on) return;
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  a = take_event();
+  b = take_event();
+  cudaEventRecord(a, s);
+}
+ProfScope::~ProfScope() {
+  if (!a) return;
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  cudaEventRecord(b, s);
+  g_pending.push_back({(int)id, a, b});
+  if (g_pending.size() > 4096) drain_pending();
+}
+
+// ------------------------------------------------------------------ pointers
+bool is_device_ptr(const void* p) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+void free_workspace(Workspace* w) { delete w; }
+
+Workspace& band_ws(const cpm_band* b) {
+  cpm_band* mb = const_cast<cpm_band*>(b);
+  if (!mb->ws) mb->ws = new Workspace();
+  return *mb->ws;
+}
+
+static int ensure_stage(const cpm_band* b) {
+  cpm_band* mb = const_cast<cpm_band*>(b);
+  if (!mb->dstage0) {
+    CPM_CUDA(cudaMalloc(&mb->dstage0, sizeof(double) * std::max<int64_t>(b->nA, 1)));
+    CPM_CUDA(cudaMalloc(&mb->dstage1, sizeof(double) * std::max<int64_t>(b->nA, 1)));
+  }
+  return CPM_OK;
+}
+
+}  // namespace cpm
+
+using namespace cpm;
+
+extern "C" {
+
+const char* cpm_version(void) { return "paper_2110_06322_b200 cpm 0.1 (sm_100a)"; }
+const char* cpm_last_error(void) { return g_err.c_str(); }
+
+int cpm_build_band(const cpm_surface* surface, double h, int p, double L, void* stream,
+                   cpm_band** out) {
+  return build_band(surface, h, p, L, (cudaStream_t)stream, out);
+}
+
+int cpm_band_get_info(const cpm_band* b, cpm_band_info* info) {
+  if (!b || !info) return fail(CPM_ERR_ARG, "cpm_band_get_info: null argument");
+  memset(info, 0, sizeof(*info));
+  info->n_active = b->nA;
+  info->n_ghost = b->nG;
+  info->n_tiles = b->nT;
+  info->n_runs = b->nRuns;
+  info->max_box = b->maxBox;
+  info->bytes_device = b->bytes;
+  info->h = b->h;
+  info->lambda = b->lam;
+  info->L = b->L;
+  for (int q = 0; q < 3; ++q) {
+    info->lattice_lo[q] = b->ilo[q];
+    info->lattice_hi[q] = b->ihi[q];
+  }
+  info->zero_fill = b->zeroFill ? 1 : 0;
+  info->rank = b->rank;
+  info->nranks = b->nranks;
+  info->n_owned = b->nOwned;
+  info->n_halo = b->nHalo;
+  return CPM_OK;
+}
+
+int cpm_band_active_coords(const cpm_band* b, int32_t* ijk_host) {
+  if (!b || !ijk_host) return fail(CPM_ERR_ARG, "cpm_band_active_coords: null argument");
+  CPM_CUDA(cudaMemcpy(ijk_host, b->aijk, sizeof(int32_t) * 3 * b->nA, cudaMemcpyDeviceToHost));
+  return CPM_OK;
+}
+
+int cpm_band_ghost_coords(const cpm_band* b, int32_t* ijk_host) {
+  if (!b || !ijk_host) return fail(CPM_ERR_ARG, "cpm_band_ghost_coords: null argument");
+  if (b->nG > 0)
+    CPM_CUDA(cudaMemcpy(ijk_host, b->gijk, sizeof(int32_t) * 3 * b->nG, cudaMemcpyDeviceToHost));
+  return CPM_OK;
+}
+
+void cpm_band_free(cpm_band* b) { free_band(b); }
+
+int cpm_apply(const cpm_band* b, double c, const double* u, double* y, void* stream) {
+  if (!b || !u || !y) return fail(CPM_ERR_ARG, "cpm_apply: null argument");
+  if ((const void*)u == (const void*)y) return fail(CPM_ERR_ARG, "cpm_apply: u and y must not alias");
+  cudaStream_t s = (cudaStream_t)stream;
+  const bool du = is_device_ptr(u), dy = is_device_ptr(y);
+  if (du && dy) return apply_device(b, c, u, y, nullptr, s);
+  CPM_TRY(ensure_stage(b));
+  const size_t bytes = sizeof(double) * b->nA;
+  const double* uu = u;
+  if (!du) {
+    CPM_CUDA(cudaMemcpyAsync(b->dstage0, u, bytes, cudaMemcpyHostToDevice, s));
+    uu = b->dstage0;
+  }
+  double* yy = dy ? y : b->dstage1;
+  CPM_TRY(apply_device(b, c, uu, yy, nullptr, s));
+  if (!dy) CPM_CUDA(cudaMemcpyAsync(y, yy, bytes, cudaMemcpyDeviceToHost, s));
+  CPM_CUDA(cudaStreamSynchronize(s));
+  return CPM_OK;
+}
+
+int cpm_solve(const cpm_band* b, double c, const double* f, double* u, double rtol, int restart,
+              int maxit, const cpm_ras* ras, cpm_solve_stats* stats, void* stream);
+
+int cpm_eval_sph(const cpm_band* b, int l, int m, double scale, double* out, void* stream) {
+  if (!b || !out) return fail(CPM_ERR_ARG, "cpm_eval_sph: null argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (is_device_ptr(out)) return eval_sph_device(b, l, m, scale, out, s);
+  CPM_TRY(ensure_stage(b));
+  CPM_TRY(eval_sph_device(b, l, m, scale, b->dstage1, s));
+  CPM_CUDA(cudaMemcpyAsync(out, b->dstage1, sizeof(double) * b->nA, cudaMemcpyDeviceToHost, s));
+  CPM_CUDA(cudaStreamSynchronize(s));
+  return CPM_OK;
+}
+
+int cpm_eval_torus_rhs(const cpm_band* b, const double* coeffs, int nq, double* out,
+                       void* stream) {
+  if (!b || !out) return fail(CPM_ERR_ARG, "cpm_eval_torus_rhs: null argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (is_device_ptr(out)) return eval_torus_device(b, coeffs, nq, out, s);
+  CPM_TRY(ensure_stage(b));
+  CPM_TRY(eval_torus_device(b, coeffs, nq, b->dstage1, s));
+  CPM_CUDA(cudaMemcpyAsync(out, b->dstage1, sizeof(double) * b->nA, cudaMemcpyDeviceToHost, s));
+  CPM_CUDA(cudaStreamSynchronize(s));
+  return CPM_OK;
+}
+
+int cpm_profile_enable(int on) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  g_prof_on = on != 0;
+  return CPM_OK;
+}
+int cpm_profile_reset(void) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  drain_pending();
+  for (int q = 0; q < K_COUNT; ++q) {
+    g_ms[q] = 0;
+    g_cnt[q] = 0;
+  }
+  return CPM_OK;
+}
+int cpm_profile_read(const char* name, double* ms, int64_t* launches) {
+  if (!name) return fail(CPM_ERR_ARG, "cpm_profile_read: null name");
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  drain_pending();
+  for (int q = 0; q < K_COUNT; ++q)
+    if (strcmp(name, g_names[q]) == 0) {
+      if (ms) *ms = g_ms[q];
+      if (launches) *launches = g_cnt[q];
+      return CPM_OK;
+    }
+  return fail(CPM_ERR_ARG, std::string("cpm_profile_read: unknown kernel name ") + name);
+}
+int64_t cpm_kernel_launches(void) { return g_launches.load(); }
+
+}  // extern "C"

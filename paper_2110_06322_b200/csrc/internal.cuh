@@ -1,0 +1,123 @@
+// internal.cuh — private definitions of the CPM CUDA library (not part of the ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/cpm.h"
+
+namespace cpm {
+
+constexpr int kBrick = 8;                 // brick edge (lattice cells)
+constexpr int kBrickCells = 512;          // 8^3
+constexpr int kMaxBoxEdge = 30;           // per-axis cap of a tile's stencil box
+constexpr int kMaxBoxCells = 12288;       // 96 KiB of doubles per tile box
+constexpr int kMortonBias = 1 << 16;      // brick coordinate bias (reading R8)
+
+// ------------------------------------------------------------------ error state
+void set_error(const std::string& msg);
+int fail(int code, const std::string& msg);
+int cuda_fail(cudaError_t e, const char* what, const char* file, int line);
+
+#define CPM_CUDA(call)                                                   \
+  do {                                                                   \
+    cudaError_t _e = (call);                                             \
+    if (_e != cudaSuccess) return ::cpm::cuda_fail(_e, #call, __FILE__, __LINE__); \
+  } while (0)
+
+#define CPM_TRY(call)             \
+  do {                            \
+    int _rc = (call);             \
+    if (_rc != CPM_OK) return _rc; \
+  } while (0)
+
+// ------------------------------------------------------------------ profiling
+// Kernel ids for cpm_profile_read.
+enum KernelId { K_EXTEND = 0, K_LAPLACE, K_MDOT, K_CGS_UPDATE, K_CGS_FINAL, K_AXPY, K_OTHER, K_COUNT };
+struct ProfScope {
+  ProfScope(KernelId id, cudaStream_t s);
+  ~ProfScope();
+  KernelId id;
+  cudaStream_t s;
+  cudaEvent_t a = nullptr, b = nullptr;
+};
+void count_launch();
+
+// ------------------------------------------------------------------ band data
+// One tile = one occupied 8^3 brick.  64-bit aligned, 96 bytes.
+struct TileHdr {
+  int32_t e0, e1;      // eval nodes (Sigma_A u Sigma_G in the brick) [e0, e1)
+  int32_t a0, a1;      // output (active / owned) nodes [a0, a1)
+  int32_t r0, r1;      // stencil-box fill runs [r0, r1)
+  int32_t ox, oy, oz;  // stencil box origin (lattice)
+  int32_t sx, sy, sz;  // stencil box extent (cells)
+  int32_t nbr[6];      // face neighbour tile slots (+x,-x,+y,-y,+z,-z), -1 = none
+  int32_t bx, by, bz;  // brick coordinates (lattice origin = 8*b)
+  int32_t pad[3];
+};
+static_assert(sizeof(TileHdr) == 96, "TileHdr layout");
+
+// A fill run copies len consecutive source doubles u[src..src+len) to
+// box[dst..dst+len).  Packed: src (bits 0-31), dst (32-47), len (48-55).
+__host__ __device__ inline uint64_t pack_run(uint32_t src, uint32_t dst, uint32_t len) {
+  return (uint64_t)src | ((uint64_t)dst << 32) | ((uint64_t)len << 48);
+}
+
+struct Surface {
+  int kind;
+  double p[4];
+};
+
+struct Workspace;  // krylov.cuh
+
+}  // namespace cpm
+
+// The band handle.  All pointers are device memory unless noted.
+struct cpm_band {
+  cpm::Surface surf;
+  double h = 0, lam = 0, L = 0;
+  int M = 0;
+  int64_t nA = 0, nG = 0, nE = 0;  // active, ghost, eval (= nA + nG for a full band)
+  int nT = 0;                      // tiles
+  int64_t nRuns = 0;
+  int maxBox = 0;
+  bool zeroFill = false;
+  int ilo[3] = {0, 0, 0}, ihi[3] = {0, 0, 0};
+  int rank = 0, nranks = 1;
+  int64_t nOwned = 0, nHalo = 0;   // partitioned bands
+
+  cpm::TileHdr* tiles = nullptr;
+  double* tx = nullptr;            // nE fractional offsets (SoA)
+  double* ty = nullptr;
+  double* tz = nullptr;
+  uint32_t* eoff = nullptr;        // nE: box offset (low 16) | brick cell (high 16)
+  uint16_t* acell = nullptr;       // nA: brick cell of each output node
+  int32_t* aijk = nullptr;         // 3*nA lattice coords (band order)
+  int32_t* gijk = nullptr;         // 3*nG lattice coords
+  uint64_t* runs = nullptr;        // nRuns fill runs
+  double* vb = nullptr;            // nT*512 scratch: E u per brick cell
+
+  // host staging for host-pointer calls
+  double* dstage0 = nullptr;       // nA
+  double* dstage1 = nullptr;       // nA
+  int64_t bytes = 0;
+  cpm::Workspace* ws = nullptr;    // cached GMRES workspace (host-owned object)
+};
+
+namespace cpm {
+// apply.cu
+int apply_device(const cpm_band* b, double c, const double* u, double* y, const double* scale,
+                 cudaStream_t s);
+// build.cu
+int build_band(const cpm_surface* surf, double h, int p, double L, cudaStream_t s, cpm_band** out);
+void free_band(cpm_band* b);
+// problems.cu
+int eval_sph_device(const cpm_band* b, int l, int m, double scale, double* out, cudaStream_t s);
+int eval_torus_device(const cpm_band* b, const double* coeffs, int nq, double* out,
+                      cudaStream_t s);
+// pointer helpers (capi.cpp)
+bool is_device_ptr(const void* p);
+}  // namespace cpm

@@ -1,0 +1,62 @@
+// krylov.cuh — device GMRES state and workspace (private).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <functional>
+
+#include "internal.cuh"
+
+namespace cpm {
+
+constexpr int kMaxRestart = 128;
+
+// Device-resident Arnoldi / Givens state of one (F)GMRES solve.
+struct GState {
+  double H[(kMaxRestart + 1) * kMaxRestart];  // column j at H[j*(m_max+1)]
+  double cs[kMaxRestart], sn[kMaxRestart];
+  double g[kMaxRestart + 1], y[kMaxRestart];
+  double sc[kMaxRestart + 1];                 // 1/||w_i|| of the stored basis vectors
+  double h1[kMaxRestart + 1], h2[kMaxRestart + 1];
+  double nrm2, beta, target;
+  int k, done, breakdown, its;                // contiguous: copied to the host together
+  double est, beta2;                          // contiguous
+  unsigned counter[8];
+};
+
+struct HostState {
+  int k, done, breakdown, its;
+  double est, beta2;
+};
+
+// y = scale * A x  (scale: device pointer or nullptr)
+struct LinOp {
+  std::function<int(const double*, double*, const double*, cudaStream_t)> apply;
+};
+// z = M r
+struct PrecOp {
+  std::function<int(const double*, double*, cudaStream_t)> apply;
+};
+
+struct Workspace {
+  int64_t n = 0, ldv = 0;
+  int m = 0;
+  bool flex = false;
+  double* V = nullptr;
+  double* Z = nullptr;
+  double* w = nullptr;
+  double* t = nullptr;
+  double* partial = nullptr;
+  GState* st = nullptr;
+  HostState* hst = nullptr;
+  int ensure(int64_t n, int m, bool flex);
+  void release();
+  ~Workspace() { release(); }
+};
+
+int gmres_device(const LinOp& A, const PrecOp* M, const double* b, double* x, int64_t n,
+                 double rtol, int m, int maxit, Workspace& ws, cpm_solve_stats* stats,
+                 cudaStream_t s);
+
+}  // namespace cpm

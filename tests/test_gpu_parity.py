@@ -1,0 +1,273 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Tolerances (north_star): one apply agrees to relative max-norm 1e-12; converged
+solutions agree to 1e-8 relative at rtol 1e-10 with iteration counts +-1.
+Integer work (band membership, ordering) is compared bit-exactly.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import seeded_inputs
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle.band import Band as OBand, node_key  # noqa: E402
+from oracle.krylov import gmres as ogmres  # noqa: E402
+from oracle.operator import apply_rows, shifted_operator  # noqa: E402
+from oracle.order import band_order_key  # noqa: E402
+from oracle.problems import exact_sph, rhs_sph, rhs_torus  # noqa: E402
+from oracle.surfaces import Sphere, Torus  # noqa: E402
+
+APPLY_TOL = 1e-12
+SOLVE_TOL = 1e-8
+
+
+@pytest.fixture(scope="module")
+def cpm():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2110_06322_b200._build import build
+
+    build()
+    import paper_2110_06322_b200 as p
+
+    return p
+
+
+def _perm_to_oracle(gpu_ijk: np.ndarray, ob: OBand) -> np.ndarray:
+    """index into the oracle's Sigma_A for each GPU node (asserts all present)."""
+    idx = ob.index_active(gpu_ijk.astype(np.int64))
+    assert np.all(idx >= 0)
+    return idx
+
+
+def _gpu_band(cpm, kind, h, **kw):
+    return cpm.cpm_build_band(kind, h, **kw)
+
+
+CASES = [("sphere", 0.1, {}), ("sphere", 0.13, {}), ("torus", 0.05, {"R": 1.0, "r": 0.4}),
+         ("sphere", 0.06, {"R": 0.7})]
+
+
+def _oracle_surface(kind, kw):
+    return Sphere(kw.get("R", 1.0)) if kind == "sphere" else Torus(kw.get("R", 1.0), kw.get("r", 0.4))
+
+
+@pytest.mark.parametrize("kind,h,kw", CASES)
+def test_band_bit_exact(cpm, kind, h, kw):
+    gb = _gpu_band(cpm, kind, h, **kw)
+    ob = OBand(_oracle_surface(kind, kw), h)
+    ga = cpm.cpm_band_active_coords(gb).astype(np.int64)
+    gg = cpm.cpm_band_ghost_coords(gb).astype(np.int64)
+    assert gb.info.n_active == ob.nA and gb.info.n_ghost == ob.nG
+    assert np.array_equal(np.sort(node_key(ga)), ob.akeys)
+    assert np.array_equal(np.sort(node_key(gg)), ob.gkeys)
+    # band order (reading R8): strictly increasing Morton-brick key
+    keys = band_order_key(ga)
+    assert np.all(np.diff(keys) > 0)
+
+
+@pytest.mark.parametrize("kind,h,kw", CASES)
+@pytest.mark.parametrize("c", [1.0, 10.0])
+def test_apply_parity(cpm, kind, h, kw, c):
+    gb = _gpu_band(cpm, kind, h, **kw)
+    ob = OBand(_oracle_surface(kind, kw), h)
+    ga = cpm.cpm_band_active_coords(gb).astype(np.int64)
+    perm = _perm_to_oracle(ga, ob)
+    u_h = seeded_inputs.uniform_pm1(0, ga)
+    u = torch.from_numpy(u_h).cuda()
+    y = torch.empty_like(u)
+    cpm.cpm_apply(gb, c, u, y)
+    torch.cuda.synchronize()
+    A = shifted_operator(ob, c)
+    u_o = np.empty(ob.nA)
+    u_o[perm] = u_h
+    y_o = (A @ u_o)[perm]
+    err = np.abs(y.cpu().numpy() - y_o).max() / np.abs(y_o).max()
+    assert err <= APPLY_TOL, err
+
+
+def test_apply_host_pointers_match_device(cpm):
+    gb = _gpu_band(cpm, "sphere", 0.1)
+    ga = cpm.cpm_band_active_coords(gb).astype(np.int64)
+    u_h = seeded_inputs.uniform_pm1(3, ga)
+    y_h = np.empty_like(u_h)
+    cpm.cpm_apply(gb, 2.0, u_h, y_h)                       # host in, host out
+    u = torch.from_numpy(u_h).cuda()
+    y = torch.empty_like(u)
+    cpm.cpm_apply(gb, 2.0, u, y)
+    torch.cuda.synchronize()
+    assert np.array_equal(y.cpu().numpy(), y_h)           # same kernels, same bits
+
+
+def test_apply_edge_cases(cpm):
+    gb = _gpu_band(cpm, "sphere", 0.1)
+    n = gb.n
+    z = torch.zeros(n, dtype=torch.float64, device="cuda")
+    y = torch.empty_like(z)
+    cpm.cpm_apply(gb, 3.0, z, y)
+    assert torch.count_nonzero(y).item() == 0
+    one = torch.ones(n, dtype=torch.float64, device="cuda")
+    cpm.cpm_apply(gb, 3.0, one, y)                         # Delta_S 1 = 0 (E rows sum to 1)
+    assert torch.max(torch.abs(y - 3.0)).item() <= 1e-12 * 6 / 0.01
+    with pytest.raises(cpm.CpmError):
+        cpm.cpm_apply(gb, 1.0, one, one)                   # aliasing rejected
+    with pytest.raises(cpm.CpmError):
+        cpm.cpm_apply(gb, 1.0, one[:-1], y)                # wrong length
+
+
+def test_band_errors(cpm):
+    with pytest.raises(cpm.CpmError, match="undefined|StencilEscape"):
+        cpm.cpm_build_band("sphere", 0.25)                 # lambda + h > reach 1
+    with pytest.raises(cpm.CpmError, match="empty|no active"):
+        cpm.cpm_build_band("sphere", 0.1, L=0.3)           # box misses the surface
+    with pytest.raises(cpm.CpmError, match="p = 3"):
+        cpm.cpm_build_band("sphere", 0.1, p=2)
+
+
+def test_solve_parity_config0(cpm):
+    """BASELINE config 0: unit sphere h=0.1, c=1, f=(c+12)Y_3^2, GMRES(30), rtol 1e-10."""
+    h, c = 0.1, 1.0
+    gb = _gpu_band(cpm, "sphere", h)
+    ob = OBand(Sphere(1.0), h)
+    ga = cpm.cpm_band_active_coords(gb).astype(np.int64)
+    perm = _perm_to_oracle(ga, ob)
+    f = torch.empty(gb.n, dtype=torch.float64, device="cuda")
+    cpm.cpm_eval_sph(gb, 3, 2, c + 12.0, f)
+    f_o = rhs_sph(ob, c, 3, 2)
+    assert np.abs(f.cpu().numpy() - f_o[perm]).max() <= 1e-13 * np.abs(f_o).max()
+    u = torch.zeros_like(f)
+    st = cpm.cpm_solve(gb, c, f, u, rtol=1e-10, restart=30)
+    A = shifted_operator(ob, c)
+    x_o, so = ogmres(lambda v: A @ v, f_o, restart=30, rtol=1e-10)
+    assert st.converged and so.converged
+    assert abs(st.iterations - so.iterations) <= 1, (st.iterations, so.iterations)
+    ug = u.cpu().numpy()
+    err = np.abs(ug - x_o[perm]).max() / np.abs(x_o).max()
+    assert err <= SOLVE_TOL, err
+    assert st.resid_true <= 1.5e-10 * st.bnorm
+    # and the discrete solution is O(h^2)-close to the manufactured solution
+    assert np.abs(ug - exact_sph(ob, 3, 2)[perm]).max() < 0.03
+
+
+@pytest.mark.parametrize("restart,its_tol", [(50, 1), (30, 1), (5, 0.10)])
+def test_solve_parity_torus(cpm, restart, its_tol):
+    """Torus R=1 r=0.4 (config 2 shape) at h=0.05.  Iteration counts must agree +-1 for
+    the BASELINE restarts; for GMRES(5) (hundreds of restart cycles) the count is
+    rounding-sensitive — the oracle itself gives 1889 on one host and 1811 on
+    another — so only a 10 % band is asserted there (parity notes)."""
+    h, c = 0.05, 1.0
+    gb = _gpu_band(cpm, "torus", h, R=1.0, r=0.4)
+    ob = OBand(Torus(1.0, 0.4), h)
+    ga = cpm.cpm_band_active_coords(gb).astype(np.int64)
+    perm = _perm_to_oracle(ga, ob)
+    f_o = rhs_torus(ob, seed=1)
+    f = torch.empty(gb.n, dtype=torch.float64, device="cuda")
+    cpm.cpm_eval_torus_rhs(gb, seeded_inputs.smooth_modulation_coeffs(1), f)
+    assert np.abs(f.cpu().numpy() - f_o[perm]).max() <= 1e-12
+    u = torch.zeros_like(f)
+    st = cpm.cpm_solve(gb, c, f, u, rtol=1e-10, restart=restart)
+    A = shifted_operator(ob, c)
+    x_o, so = ogmres(lambda v: A @ v, f_o, restart=restart, rtol=1e-10)
+    assert st.converged and so.converged
+    if isinstance(its_tol, int):
+        assert abs(st.iterations - so.iterations) <= its_tol, (st.iterations, so.iterations)
+    else:
+        assert abs(st.iterations - so.iterations) <= its_tol * so.iterations, (st.iterations, so.iterations)
+    err = np.abs(u.cpu().numpy() - x_o[perm]).max() / np.abs(x_o).max()
+    assert err <= SOLVE_TOL, err
+
+
+def test_solve_host_pointers_and_x0(cpm):
+    gb = _gpu_band(cpm, "sphere", 0.1)
+    f = np.empty(gb.n)
+    cpm.cpm_eval_sph(gb, 3, 2, 13.0, f)
+    u = np.zeros(gb.n)
+    st = cpm.cpm_solve(gb, 1.0, f, u, rtol=1e-10, restart=30)
+    assert st.converged
+    st2 = cpm.cpm_solve(gb, 1.0, f, u.copy(), rtol=1e-10, restart=30)   # x0 = solution
+    assert st2.iterations <= 3
+
+
+# ------------------------------------------------------------------ full size (config 1)
+@pytest.fixture(scope="module")
+def big(cpm):
+    gb = cpm.cpm_build_band("sphere", 1.0 / 200)
+    return gb
+
+
+def test_full_size_band_count(cpm, big):
+    """config 1 band, h=1/200: node count against the oracle's own enumeration."""
+    ob = OBand(Sphere(1.0), 1.0 / 200)
+    assert big.info.n_active == ob.nA and big.info.n_ghost == ob.nG
+    ga = cpm.cpm_band_active_coords(big).astype(np.int64)
+    assert np.array_equal(np.sort(node_key(ga)), ob.akeys)
+
+
+def test_full_size_apply_sampled(cpm, big):
+    """config 1 apply (u ~ U[-1,1], seed 0) on 3000 sampled rows vs the oracle's row formula."""
+    h = 1.0 / 200
+    ga = cpm.cpm_band_active_coords(big).astype(np.int64)
+    u = torch.from_numpy(seeded_inputs.uniform_pm1(0, ga)).cuda()
+    y = torch.empty_like(u)
+    cpm.cpm_apply(big, 10.0, u, y)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(11)
+    sel = np.concatenate([rng.choice(big.n, 2990, replace=False), np.arange(5), big.n - 1 - np.arange(5)])
+
+    class _B:
+        pass
+
+    _B.h = h
+    _B.surface = Sphere(1.0)
+    y_o = apply_rows(_B, 10.0, lambda q: seeded_inputs.uniform_pm1(0, q), ga[sel])
+    yg = y.cpu().numpy()
+    err = np.abs(yg[sel] - y_o).max() / np.abs(y_o).max()
+    assert err <= APPLY_TOL, err
+    # property at any size: constants are in the kernel of Delta_S^h
+    one = torch.ones_like(u)
+    cpm.cpm_apply(big, 10.0, one, y)
+    assert torch.max(torch.abs(y - 10.0)).item() <= 1e-11 * 6 * 200 ** 2
+
+
+def test_full_size_manufactured_solve(cpm, big):
+    """config 1 solve: c=10, f=(c+42)Y_6^3, GMRES(50), rtol 1e-10: converges; residual
+    recomputed by the oracle row formula on samples; O(h^2) error vs Y_6^3(cp)."""
+    h, c = 1.0 / 200, 10.0
+    f = torch.empty(big.n, dtype=torch.float64, device="cuda")
+    cpm.cpm_eval_sph(big, 6, 3, c + 42.0, f)
+    u = torch.zeros_like(f)
+    st = cpm.cpm_solve(big, c, f, u, rtol=1e-10, restart=50)
+    assert st.converged
+    assert st.resid_true <= 2e-10 * st.bnorm
+    ga = cpm.cpm_band_active_coords(big).astype(np.int64)
+    ug = u.cpu().numpy()
+    ob_s = Sphere(1.0)
+
+    class _B:
+        pass
+
+    _B.h = h
+    _B.surface = ob_s
+    from oracle.sph import real_sph
+
+    x = ga.astype(np.float64) * h
+    cp, _ = ob_s.cp(x)
+    exact = real_sph(6, 3, cp)
+    assert np.abs(ug - exact).max() < 5e-3
+    # oracle residual on sampled rows: u looked up by lattice coordinate
+    keys = node_key(ga)
+    order = np.argsort(keys)
+    sk = keys[order]
+
+    def u_of(q):
+        pos = np.searchsorted(sk, node_key(q))
+        assert np.all(sk[pos] == node_key(q))
+        return ug[order[pos]]
+
+    sel = np.random.default_rng(2).choice(big.n, 500, replace=False)
+    fr = f.cpu().numpy()[sel] - apply_rows(_B, c, u_of, ga[sel])
+    assert np.abs(fr).max() <= 1e-6 * np.abs(f.cpu().numpy()).max()
