@@ -147,6 +147,53 @@ int cpm_ras_setup(const cpm_band* band, int n_sub, int overlap, int k_inner, dou
 int cpm_ras_apply(const cpm_ras* ras, const double* r, double* z, void* stream);
 void cpm_ras_free(cpm_ras* ras);
 
+/* ---------------------------------------------------------------- multi-GPU (north_star item 5)
+ * One process per GPU.  Every rank builds the same global band (deterministic,
+ * cheap) and then its partition: rank r of R owns the band-order slab
+ * [floor(r nA/R), floor((r+1) nA/R)) (reading R8); its local operator reads the
+ * owned entries of a vector plus a HALO of other ranks' entries (the active nodes
+ * in the stencil boxes of the tiles it evaluates).  Before every apply the halo
+ * is exchanged with NCCL send/recv; every Krylov reduction is an NCCL allreduce.
+ * NCCL is loaded at run time (dlopen "libnccl.so.2"); without it the cpm_comm_*
+ * calls return CPM_ERR_NCCL and the single-GPU API is unaffected. */
+typedef struct cpm_part cpm_part;
+typedef struct cpm_part_info {
+  int32_t rank, nranks;
+  int64_t lo, hi;        /* owned band-order range [lo, hi) */
+  int64_t n_owned, n_halo, n_tiles, n_send;
+} cpm_part_info;
+
+/* 128-byte NCCL unique id (rank 0 creates it; broadcast it, e.g. with torch.distributed). */
+int cpm_comm_unique_id(void* id_out_128);
+int cpm_comm_init(const void* id_128, int rank, int nranks, cpm_comm** out);
+void cpm_comm_free(cpm_comm* comm);
+
+/* Build rank's partition of `band` (device work on stream).  Errors: CPM_ERR_ARG. */
+int cpm_part_create(const cpm_band* band, int rank, int nranks, void* stream, cpm_part** out);
+int cpm_part_get_info(const cpm_part* part, cpm_part_info* info);
+/* Global band-order indices of the halo nodes (sorted ascending, grouped by owner
+ * rank) into a HOST int64 array of n_halo entries: what this rank RECEIVES. */
+int cpm_part_halo_nodes(const cpm_part* part, int64_t* halo_host);
+/* What this rank SENDS: for every peer q (counts[q] entries, peers in rank order)
+ * the owned global indices peer q requested (its cpm_part_halo_nodes restricted to
+ * this rank's slab, in its order).  HOST arrays; copied.  Errors: CPM_ERR_ARG if an
+ * index is not owned. */
+int cpm_part_set_send(cpm_part* part, const int64_t* send_global_host, const int64_t* counts_host);
+/* y_owned = (c - Delta_S^h) u restricted to the owned rows, halo values given
+ * explicitly (u_halo: n_halo doubles in cpm_part_halo_nodes order); no
+ * communication.  Device pointers. */
+int cpm_part_apply_local(const cpm_part* part, double c, const double* u_owned,
+                         const double* u_halo, double* y_owned, void* stream);
+/* Halo exchange over `comm` + local apply.  Device pointers (n_owned doubles). */
+int cpm_part_apply(const cpm_part* part, const cpm_comm* comm, double c, const double* u_owned,
+                   double* y_owned, void* stream);
+/* Distributed GMRES(restart) on the owned slices (conventions of cpm_solve); every
+ * rank gets identical statistics. */
+int cpm_part_solve(const cpm_part* part, const cpm_comm* comm, double c, const double* f_owned,
+                   double* u_owned, double rtol, int restart, int maxit, cpm_solve_stats* stats,
+                   void* stream);
+void cpm_part_free(cpm_part* part);
+
 /* ---------------------------------------------------------------- problem data
  * cpm_eval_sph — out_i = scale * Y_l^m(cp(x_i)) on the active nodes, real
  * orthonormal spherical harmonics without Condon-Shortley phase (reading R9);

@@ -88,6 +88,18 @@ _SIGS = {
     "cpm_profile_read": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(ctypes.c_double),
                                         ctypes.POINTER(ctypes.c_int64)]),
     "cpm_kernel_launches": (ctypes.c_int64, []),
+    "cpm_comm_unique_id": (ctypes.c_int, [_vp]),
+    "cpm_comm_init": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, ctypes.POINTER(_vp)]),
+    "cpm_comm_free": (None, [_vp]),
+    "cpm_part_create": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, _vp, ctypes.POINTER(_vp)]),
+    "cpm_part_get_info": (ctypes.c_int, [_vp, _vp]),
+    "cpm_part_halo_nodes": (ctypes.c_int, [_vp, _vp]),
+    "cpm_part_set_send": (ctypes.c_int, [_vp, _vp, _vp]),
+    "cpm_part_apply_local": (ctypes.c_int, [_vp, ctypes.c_double, _vp, _vp, _vp, _vp]),
+    "cpm_part_apply": (ctypes.c_int, [_vp, _vp, ctypes.c_double, _vp, _vp, _vp]),
+    "cpm_part_solve": (ctypes.c_int, [_vp, _vp, ctypes.c_double, _vp, _vp, ctypes.c_double, ctypes.c_int,
+                                      ctypes.c_int, ctypes.POINTER(_SolveStats), _vp]),
+    "cpm_part_free": (None, [_vp]),
 }
 
 _lib = None
@@ -328,3 +340,129 @@ def cpm_kernel_launches() -> int:
 
 def cpm_version() -> str:
     return load_library().cpm_version().decode()
+
+
+# ---------------------------------------------------------------- multi-GPU
+class _PartInfo(ctypes.Structure):
+    _fields_ = [("rank", ctypes.c_int32), ("nranks", ctypes.c_int32), ("lo", ctypes.c_int64),
+                ("hi", ctypes.c_int64), ("n_owned", ctypes.c_int64), ("n_halo", ctypes.c_int64),
+                ("n_tiles", ctypes.c_int64), ("n_send", ctypes.c_int64)]
+
+
+class Part:
+    """Owning wrapper of a cpm_part handle (this rank's slab of a band)."""
+
+    def __init__(self, handle, band: Band):
+        self._h = handle
+        self.band = band
+        self.refresh()
+
+    def refresh(self):
+        inf = _PartInfo()
+        _check(load_library().cpm_part_get_info(self._h, ctypes.byref(inf)), "cpm_part_get_info")
+        self.rank, self.nranks = inf.rank, inf.nranks
+        self.lo, self.hi = inf.lo, inf.hi
+        self.n_owned, self.n_halo, self.n_tiles, self.n_send = inf.n_owned, inf.n_halo, inf.n_tiles, inf.n_send
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self):
+        if self._h:
+            load_library().cpm_part_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Comm:
+    def __init__(self, handle):
+        self._h = handle
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self):
+        if self._h:
+            load_library().cpm_comm_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def cpm_comm_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(load_library().cpm_comm_unique_id(buf), "cpm_comm_unique_id")
+    return buf.raw
+
+
+def cpm_comm_init(uid: bytes, rank: int, nranks: int) -> Comm:
+    buf = ctypes.create_string_buffer(uid, 128)
+    out = _vp()
+    _check(load_library().cpm_comm_init(buf, int(rank), int(nranks), ctypes.byref(out)), "cpm_comm_init")
+    return Comm(out)
+
+
+def cpm_part_create(band: Band, rank: int, nranks: int, stream=None) -> Part:
+    out = _vp()
+    _check(load_library().cpm_part_create(band.handle, int(rank), int(nranks), stream, ctypes.byref(out)),
+           "cpm_part_create")
+    return Part(out, band)
+
+
+def cpm_part_halo_nodes(part: Part) -> np.ndarray:
+    out = np.empty(part.n_halo, dtype=np.int64)
+    _check(load_library().cpm_part_halo_nodes(part.handle, out.ctypes.data if part.n_halo else None),
+           "cpm_part_halo_nodes")
+    return out
+
+
+def cpm_part_set_send(part: Part, send_global: np.ndarray, counts: np.ndarray):
+    sg = np.ascontiguousarray(send_global, dtype=np.int64)
+    ct = np.ascontiguousarray(counts, dtype=np.int64)
+    if ct.size != part.nranks or sg.size != int(ct.sum()):
+        raise CpmError("cpm_part_set_send: counts must have nranks entries summing to len(send_global)")
+    _check(load_library().cpm_part_set_send(part.handle, sg.ctypes.data if sg.size else None, ct.ctypes.data),
+           "cpm_part_set_send")
+    part.refresh()
+
+
+def cpm_part_apply_local(part: Part, c: float, u_owned, u_halo, y_owned, stream=None):
+    pu, su = _ptr_stream(u_owned, part.n_owned, False)
+    ph = None
+    if part.n_halo:
+        ph, _ = _ptr_stream(u_halo, part.n_halo, False)
+    py, _ = _ptr_stream(y_owned, part.n_owned, True)
+    _check(load_library().cpm_part_apply_local(part.handle, float(c), pu, ph, py, stream or su),
+           "cpm_part_apply_local")
+    return y_owned
+
+
+def cpm_part_apply(part: Part, comm: Comm, c: float, u_owned, y_owned, stream=None):
+    pu, su = _ptr_stream(u_owned, part.n_owned, False)
+    py, _ = _ptr_stream(y_owned, part.n_owned, True)
+    _check(load_library().cpm_part_apply(part.handle, comm.handle if comm else None, float(c), pu, py,
+                                         stream or su), "cpm_part_apply")
+    return y_owned
+
+
+def cpm_part_solve(part: Part, comm: Comm, c: float, f_owned, u_owned, rtol: float = 1e-10,
+                   restart: int = 30, maxit: int = 100000, stream=None) -> SolveStats:
+    pf, sf = _ptr_stream(f_owned, part.n_owned, False)
+    pu, _ = _ptr_stream(u_owned, part.n_owned, True)
+    st = _SolveStats()
+    _check(load_library().cpm_part_solve(part.handle, comm.handle if comm else None, float(c), pf, pu,
+                                         float(rtol), int(restart), int(maxit), ctypes.byref(st), stream or sf),
+           "cpm_part_solve")
+    return SolveStats(st.iterations, bool(st.converged), st.cycles, bool(st.breakdown), st.resid_est,
+                      st.resid_true, st.bnorm, st.seconds)

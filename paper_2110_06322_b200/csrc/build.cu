@@ -243,7 +243,30 @@ __global__ void __launch_bounds__(256) k_tile_box(int nT, TileHdr* tiles, const 
     T.sx = res[3] - res[0] + 4;
     T.sy = res[4] - res[1] + 4;
     T.sz = res[5] - res[2] + 4;
-    int cells = T.sx * T.sy * T.sz;
+    // padded strides: pick row stride px >= sx and plane stride pxy >= px*sy whose
+    // small neighbour offsets fall in distinct double-banks (mod 16), so the
+    // sorted stencil gathers of one warp rarely bank-conflict.
+    int best = INT_MAX, bpx = T.sx, bpxy = T.sx * T.sy;
+    for (int dx = 0; dx < 16; ++dx)
+      for (int dz = 0; dz < 16; ++dz) {
+        const int px = T.sx + dx, pxy = px * T.sy + dz;
+        const int d[9] = {1, px, pxy, px + 1, px - 1, pxy + 1, pxy - 1, pxy + px, pxy - px};
+        int score = 0;
+        for (int a = 0; a < 9; ++a) {
+          if ((d[a] & 15) == 0) score += 16;
+          for (int b = a + 1; b < 9; ++b)
+            if (((d[a] - d[b]) & 15) == 0) score += 1;
+        }
+        score = score * 100000 + pxy * T.sz;
+        if (score < best) {
+          best = score;
+          bpx = px;
+          bpxy = pxy;
+        }
+      }
+    T.pad[0] = bpx;
+    T.pad[1] = bpxy;
+    int cells = bpxy * T.sz;
     if (T.sx > kMaxBoxEdge || T.sy > kMaxBoxEdge || T.sz > kMaxBoxEdge || cells > kMaxBoxCells)
       atomicOr(err, 2);
     atomicMax(maxbox, cells);
@@ -266,7 +289,7 @@ __global__ void k_eoff(int nT, const TileHdr* tiles, const int32_t* ebase, const
   const TileHdr T = tiles[t];
   for (int e = T.e0 + threadIdx.x; e < T.e1; e += blockDim.x) {
     int b0 = ebase[3 * (size_t)e], b1 = ebase[3 * (size_t)e + 1], b2 = ebase[3 * (size_t)e + 2];
-    uint32_t off = (uint32_t)((b0 - T.ox) + T.sx * ((b1 - T.oy) + T.sy * (b2 - T.oz)));
+    uint32_t off = (uint32_t)((b0 - T.ox) + T.pad[0] * (b1 - T.oy) + T.pad[1] * (b2 - T.oz));
     eoff[e] = off | ((uint32_t)ecell[e] << 16);
     bool ok = true;
     for (int cz = 0; cz < 4 && ok; ++cz)
@@ -282,6 +305,49 @@ __global__ void k_eoff(int nT, const TileHdr* tiles, const int32_t* ebase, const
           if (!mask_has(tam + (size_t)s * 16, cell)) ok = false;
         }
     if (!ok) atomicOr(err, 4);
+  }
+}
+
+// ------------------------------------------------------------------ B6b
+// Sort each tile's eval nodes by stencil-box offset (bitonic, <= 512 per tile) so
+// that lanes of a warp gather overlapping stencils (shared-memory broadcast).
+__global__ void __launch_bounds__(512) k_sort_tile(const TileHdr* tiles, double* tx, double* ty,
+                                                   double* tz, uint32_t* eoff) {
+  __shared__ uint32_t key[512];
+  __shared__ double sv[3][512];
+  __shared__ uint32_t so[512];
+  const TileHdr T = tiles[blockIdx.x];
+  const int n = T.e1 - T.e0, t = threadIdx.x;
+  if (t < n) {
+    const uint32_t eo = eoff[T.e0 + t];
+    key[t] = ((eo & 0xffffu) << 9) | (uint32_t)t;
+    sv[0][t] = tx[T.e0 + t];
+    sv[1][t] = ty[T.e0 + t];
+    sv[2][t] = tz[T.e0 + t];
+    so[t] = eo;
+  } else {
+    key[t] = 0xffffffffu;
+  }
+  __syncthreads();
+  for (int size = 2; size <= 512; size <<= 1)
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      const int p = t ^ stride;
+      if (p > t) {
+        const bool up = (t & size) == 0;
+        const uint32_t a = key[t], b = key[p];
+        if ((a > b) == up) {
+          key[t] = b;
+          key[p] = a;
+        }
+      }
+      __syncthreads();
+    }
+  if (t < n) {
+    const int o = key[t] & 511u;
+    tx[T.e0 + t] = sv[0][o];
+    ty[T.e0 + t] = sv[1][o];
+    tz[T.e0 + t] = sv[2][o];
+    eoff[T.e0 + t] = so[o];
   }
 }
 
@@ -325,8 +391,7 @@ __global__ void k_runs(const TileHdr* tiles, const uint32_t* tam, const int* bma
           while (q < lxe && mask_has(m, q + 8 * ly + 64 * lz)) ++q;
           if (WRITE) {
             uint32_t src = (uint32_t)(tiles[s].a0 + mask_rank(m, q0 + 8 * ly + 64 * lz));
-            uint32_t dst =
-                (uint32_t)((bx * 8 + q0 - T.ox) + T.sx * ((y - T.oy) + T.sy * (z - T.oz)));
+            uint32_t dst = (uint32_t)((bx * 8 + q0 - T.ox) + T.pad[0] * (y - T.oy) + T.pad[1] * (z - T.oz));
             runs[out + n] = pack_run(src, dst, (uint32_t)(q - q0));
           }
           ++n;
@@ -358,6 +423,16 @@ struct DevBuf {
   ~DevBuf() {
     if (p) cudaFree(p);
   }
+  template <class T>
+  T* as() {
+    return (T*)p;
+  }
+};
+
+// non-owning view with the DevBuf accessor
+template <class E>
+struct PtrView {
+  E* p;
   template <class T>
   T* as() {
     return (T*)p;
@@ -405,10 +480,16 @@ void free_workspace(Workspace* w);
 void free_band(cpm_band* b) {
   if (!b) return;
   if (b->ws) free_workspace(b->ws);
-  void* ptrs[] = {b->tiles, b->tx,  b->ty,   b->tz, b->eoff, b->acell, b->aijk,
-                  b->gijk,  b->runs, b->vb, b->dstage0, b->dstage1};
-  for (void* p : ptrs)
-    if (p) cudaFree(p);
+  if (b->owns) {
+    void* ptrs[] = {b->tiles, b->tx, b->ty,      b->tz,      b->eoff,  b->acell, b->aijk,
+                    b->gijk,  b->runs, b->vb, b->dstage0, b->dstage1, b->amask, b->bmap};
+    for (void* p : ptrs)
+      if (p) cudaFree(p);
+  } else {  // sub-band: owns only its own tiles/runs/acell/vb
+    void* ptrs[] = {b->tiles, b->runs, b->vb, b->acell, b->dstage0, b->dstage1};
+    for (void* p : ptrs)
+      if (p) cudaFree(p);
+  }
   delete b;
 }
 
@@ -526,9 +607,10 @@ int build_band(const cpm_surface* surf, double h, int p, double L, cudaStream_t 
     B->ilo[q] = ilo[q];
     B->ihi[q] = ihi[q];
   }
-  DevBuf tam, tgm, tgstart;
+  DevBuf tgm, tgstart;
   CPM_TRY(dalloc_owned(&B->tiles, totT, &B->bytes, "tiles"));
-  CPM_TRY(dalloc<uint32_t>(tam, (size_t)totT * 16, "tile amask"));
+  CPM_TRY(dalloc_owned(&B->amask, (size_t)totT * 16, &B->bytes, "tile amask"));
+  PtrView<uint32_t> tam{B->amask};
   CPM_TRY(dalloc<uint32_t>(tgm, (size_t)totT * 16, "tile gmask"));
   CPM_TRY(dalloc<int>(tgstart, totT, "tile gstart"));
   k_compact_tiles<<<grid_for(nb, 256), 256, 0, s>>>(
@@ -558,8 +640,13 @@ int build_band(const cpm_surface* surf, double h, int p, double L, cudaStream_t 
   CPM_CUDA(cudaGetLastError());
 
   // B6 brick map, boxes, offsets, coverage
-  DevBuf bmap, dblo, dbdim;
-  CPM_TRY(dalloc<int>(bmap, nbox, "brick map"));
+  DevBuf dblo, dbdim;
+  CPM_TRY(dalloc_owned(&B->bmap, nbox, &B->bytes, "brick map"));
+  for (int q = 0; q < 3; ++q) {
+    B->blo[q] = P.blo[q];
+    B->bdim[q] = P.bdim[q];
+  }
+  PtrView<int> bmap{B->bmap};
   CPM_TRY(dalloc<int>(dblo, 3, "blo"));
   CPM_TRY(dalloc<int>(dbdim, 3, "bdim"));
   CPM_CUDA(cudaMemcpyAsync(dblo.p, P.blo, 3 * sizeof(int), cudaMemcpyHostToDevice, s));
@@ -588,6 +675,9 @@ int build_band(const cpm_surface* surf, double h, int p, double L, cudaStream_t 
   if (herr[0] & 4)
     return fail(CPM_ERR_GEOM, "cpm_build_band: StencilEscape — an interpolation stencil leaves Sigma_A");
   B->maxBox = herr[1];
+  k_sort_tile<<<totT, 512, 0, s>>>(B->tiles, B->tx, B->ty, B->tz, B->eoff);
+  count_launch();
+  CPM_CUDA(cudaGetLastError());
 
   // B7 fill runs
   DevBuf nrows, rowbase, rowcnt, runstart;

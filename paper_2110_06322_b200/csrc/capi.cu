@@ -169,7 +169,7 @@ int cpm_apply(const cpm_band* b, double c, const double* u, double* y, void* str
   if ((const void*)u == (const void*)y) return fail(CPM_ERR_ARG, "cpm_apply: u and y must not alias");
   cudaStream_t s = (cudaStream_t)stream;
   const bool du = is_device_ptr(u), dy = is_device_ptr(y);
-  if (du && dy) return apply_device(b, c, u, y, nullptr, s);
+  if (du && dy) return apply_device(b, c, u, y, nullptr, 0, s);
   CPM_TRY(ensure_stage(b));
   const size_t bytes = sizeof(double) * b->nA;
   const double* uu = u;
@@ -178,7 +178,7 @@ int cpm_apply(const cpm_band* b, double c, const double* u, double* y, void* str
     uu = b->dstage0;
   }
   double* yy = dy ? y : b->dstage1;
-  CPM_TRY(apply_device(b, c, uu, yy, nullptr, s));
+  CPM_TRY(apply_device(b, c, uu, yy, nullptr, 0, s));
   if (!dy) CPM_CUDA(cudaMemcpyAsync(y, yy, bytes, cudaMemcpyDeviceToHost, s));
   CPM_CUDA(cudaStreamSynchronize(s));
   return CPM_OK;

@@ -99,6 +99,11 @@ struct cpm_band {
   int32_t* gijk = nullptr;         // 3*nG lattice coords
   uint64_t* runs = nullptr;        // nRuns fill runs
   double* vb = nullptr;            // nT*512 scratch: E u per brick cell
+  uint32_t* amask = nullptr;       // nT*16: Sigma_A occupancy bits of each tile's brick
+  int* bmap = nullptr;             // dense brick map over the brick box -> tile slot or -1
+  int blo[3] = {0, 0, 0}, bdim[3] = {0, 0, 0};
+  bool owns = true;                // false for sub-bands sharing the eval arrays
+  uint32_t srcSplit = 0xffffffffu; // fill-run sources >= srcSplit read the halo buffer
 
   // host staging for host-pointer calls
   double* dstage0 = nullptr;       // nA
@@ -109,8 +114,13 @@ struct cpm_band {
 
 namespace cpm {
 // apply.cu
+// y = scale_seg * (c - Delta_S^h) u ; scale (device, may be null) is read at
+// scale[seg * lds] with seg = the tile's segment id (0 for a plain band).
 int apply_device(const cpm_band* b, double c, const double* u, double* y, const double* scale,
-                 cudaStream_t s);
+                 int lds, cudaStream_t s);
+// as apply_device, with fill-run sources >= b->srcSplit read from uh[src - srcSplit]
+int apply_device_split(const cpm_band* b, double c, const double* u, const double* uh, double* y,
+                       const double* scale, int lds, cudaStream_t s);
 // build.cu
 int build_band(const cpm_surface* surf, double h, int p, double L, cudaStream_t s, cpm_band** out);
 void free_band(cpm_band* b);

@@ -26,245 +26,58 @@
 
 #include "internal.cuh"
 #include "krylov.cuh"
+#include "vecops.cuh"
 
 namespace cpm {
+
+// ---------------------------------------------------------------- launch helpers
 namespace {
+inline int kmax_bucket(int k) { return k <= 8 ? 8 : k <= 16 ? 16 : k <= 32 ? 32 : 64; }
+constexpr int VB = vec::VB;
+}  // namespace
 
-constexpr int VB = 256;                 // threads per block, vector kernels
-constexpr int SUB = 256;                // elements per sub-chunk
-constexpr int NQ = (kMaxRestart + 1 + 7) / 8;
-
-__device__ __forceinline__ double warp_sum(double v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
+int launch_mdot(const vec::Seg& S, int k, const double* V, int64_t ldv, const double* w,
+                const double* sc, int lds, double* partial, double* out, int ldo,
+                unsigned* counters, cudaStream_t st) {
+  vec::k_mdot8<<<S.nseg * S.gps, VB, 0, st>>>(S, k, V, ldv, w, sc, lds, partial, kMaxRestart + 8,
+                                              out, ldo, counters);
+  count_launch();
+  CPM_CUDA(cudaGetLastError());
+  return CPM_OK;
 }
 
-// Block-sum of one value per thread (deterministic order).
-__device__ double block_sum(double v) {
-  __shared__ double sw[VB / 32];
-  v = warp_sum(v);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (lane == 0) sw[warp] = v;
-  __syncthreads();
-  double r = 0.0;
-  if (warp == 0) {
-    r = lane < VB / 32 ? sw[lane] : 0.0;
-    r = warp_sum(r);
-  }
-  __syncthreads();
-  return r;  // valid in thread 0
+int launch_cgs_final(const vec::Seg& S, int k, const double* V, int64_t ldv, const double* w,
+                     const double* sc, int lds, const double* coef, int ldo, double* vout,
+                     double* partial, double* out, int ldn, unsigned* counters, cudaStream_t st) {
+  vec::k_cgs_final<<<S.nseg * S.gps, VB, 0, st>>>(S, k, V, ldv, w, sc, lds, coef, ldo, vout, partial,
+                                                  out, ldn, counters);
+  count_launch();
+  CPM_CUDA(cudaGetLastError());
+  return CPM_OK;
 }
 
-// Last block: out[i] = scale_i * sum_b partial[b * k + i], i < k.
-__device__ void last_block_finish(const double* partial, int k, const double* sc, double* out,
-                                  unsigned* counter) {
-  __shared__ bool last;
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) last = (atomicAdd(counter, 1u) == gridDim.x - 1);
-  __syncthreads();
-  if (!last) return;
-  __threadfence();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int i = warp; i < k; i += VB / 32) {
-    double a = 0.0;
-    for (int b = lane; b < (int)gridDim.x; b += 32) a += __ldcg(partial + (size_t)b * k + i);
-    a = warp_sum(a);
-    if (lane == 0) out[i] = sc ? a * sc[i] : a;
-  }
-  if (threadIdx.x == 0) *counter = 0u;
-}
-
-// ---------------------------------------------------------------- mdot: out_i = sc_i <V_i, w>
-__global__ void __launch_bounds__(VB) k_mdot(int64_t n, int k, const double* __restrict__ V,
-                                             int64_t ldv, const double* __restrict__ w,
-                                             const double* __restrict__ sc, double* partial,
-                                             double* out, unsigned* counter) {
-  __shared__ double ws[SUB];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double acc[NQ];
-#pragma unroll
-  for (int q = 0; q < NQ; ++q) acc[q] = 0.0;
-  const int64_t nsub = (n + SUB - 1) / SUB;
-  for (int64_t s = blockIdx.x; s < nsub; s += gridDim.x) {
-    const int64_t base = s * SUB;
-    const int64_t e = base + threadIdx.x;
-    ws[threadIdx.x] = e < n ? __ldg(w + e) : 0.0;
-    __syncthreads();
-    const int lim = (int)((n - base) < SUB ? (n - base) : SUB);
-#pragma unroll
-    for (int q = 0; q < NQ; ++q) {
-      const int i = warp + 8 * q;
-      if (i < k) {
-        const double* vi = V + (size_t)i * ldv + base;
-        double a0 = 0.0, a1 = 0.0;
-#pragma unroll
-        for (int r = 0; r < SUB / 32; r += 2) {
-          const int l0 = lane + 32 * r, l1 = l0 + 32;
-          if (l0 < lim) a0 += __ldg(vi + l0) * ws[l0];
-          if (l1 < lim) a1 += __ldg(vi + l1) * ws[l1];
-        }
-        acc[q] += a0 + a1;
-      }
-    }
-    __syncthreads();
-  }
-#pragma unroll
-  for (int q = 0; q < NQ; ++q) {
-    const int i = warp + 8 * q;
-    if (i < k) {
-      const double v = warp_sum(acc[q]);
-      if (lane == 0) partial[(size_t)blockIdx.x * k + i] = v;
+int launch_cgs_update(const vec::Seg& S, int k, const double* V, int64_t ldv, double* w,
+                      const double* sc, int lds, const double* coef, double* partial, double* out,
+                      int ldo, unsigned* counters, cudaStream_t st) {
+  const int grid = S.nseg * S.gps;
+  switch (k <= 64 ? kmax_bucket(k) : 0) {
+    case 8: vec::k_cgs_update<8><<<grid, VB, 0, st>>>(S, k, V, ldv, w, sc, lds, coef, partial, out, ldo, counters); break;
+    case 16: vec::k_cgs_update<16><<<grid, VB, 0, st>>>(S, k, V, ldv, w, sc, lds, coef, partial, out, ldo, counters); break;
+    case 32: vec::k_cgs_update<32><<<grid, VB, 0, st>>>(S, k, V, ldv, w, sc, lds, coef, partial, out, ldo, counters); break;
+    case 64: vec::k_cgs_update<64><<<grid, VB, 0, st>>>(S, k, V, ldv, w, sc, lds, coef, partial, out, ldo, counters); break;
+    default: {
+      // k > 64: separate update (norm into a scratch slot) and dots
+      double* scratch = out + k;  // caller guarantees room for one extra value per segment
+      CPM_TRY(launch_cgs_final(S, k, V, ldv, w, sc, lds, coef, ldo, w, partial, scratch, ldo, counters, st));
+      return launch_mdot(S, k, V, ldv, w, sc, lds, partial, out, ldo, counters, st);
     }
   }
-  last_block_finish(partial, k, sc, out, counter);
+  count_launch();
+  CPM_CUDA(cudaGetLastError());
+  return CPM_OK;
 }
 
-// ---------------------------------------------------------------- cgs_update
-// w <- w - sum_i coef_i sc_i V_i   and   out_i = sc_i <V_i, w_new>.
-__global__ void __launch_bounds__(VB) k_cgs_update(int64_t n, int k, const double* __restrict__ V,
-                                                   int64_t ldv, double* __restrict__ w,
-                                                   const double* __restrict__ sc,
-                                                   const double* __restrict__ coef,
-                                                   double* partial, double* out,
-                                                   unsigned* counter) {
-  __shared__ double ws[SUB];
-  __shared__ double cf[kMaxRestart + 1];
-  for (int i = threadIdx.x; i < k; i += VB) cf[i] = coef[i] * sc[i];
-  __syncthreads();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double acc[NQ];
-#pragma unroll
-  for (int q = 0; q < NQ; ++q) acc[q] = 0.0;
-  const int64_t nsub = (n + SUB - 1) / SUB;
-  for (int64_t s = blockIdx.x; s < nsub; s += gridDim.x) {
-    const int64_t base = s * SUB;
-    const int64_t e = base + threadIdx.x;
-    double v = 0.0;
-    if (e < n) {
-      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-      int i = 0;
-      for (; i + 3 < k; i += 4) {
-        s0 += cf[i] * __ldg(V + (size_t)i * ldv + e);
-        s1 += cf[i + 1] * __ldg(V + (size_t)(i + 1) * ldv + e);
-        s2 += cf[i + 2] * __ldg(V + (size_t)(i + 2) * ldv + e);
-        s3 += cf[i + 3] * __ldg(V + (size_t)(i + 3) * ldv + e);
-      }
-      for (; i < k; ++i) s0 += cf[i] * __ldg(V + (size_t)i * ldv + e);
-      v = w[e] - ((s0 + s1) + (s2 + s3));
-      w[e] = v;
-    }
-    ws[threadIdx.x] = v;
-    __syncthreads();
-    const int lim = (int)((n - base) < SUB ? (n - base) : SUB);
-#pragma unroll
-    for (int q = 0; q < NQ; ++q) {
-      const int i = warp + 8 * q;
-      if (i < k) {
-        const double* vi = V + (size_t)i * ldv + base;
-        double a0 = 0.0, a1 = 0.0;
-#pragma unroll
-        for (int r = 0; r < SUB / 32; r += 2) {
-          const int l0 = lane + 32 * r, l1 = l0 + 32;
-          if (l0 < lim) a0 += __ldg(vi + l0) * ws[l0];
-          if (l1 < lim) a1 += __ldg(vi + l1) * ws[l1];
-        }
-        acc[q] += a0 + a1;
-      }
-    }
-    __syncthreads();
-  }
-#pragma unroll
-  for (int q = 0; q < NQ; ++q) {
-    const int i = warp + 8 * q;
-    if (i < k) {
-      const double v = warp_sum(acc[q]);
-      if (lane == 0) partial[(size_t)blockIdx.x * k + i] = v;
-    }
-  }
-  last_block_finish(partial, k, sc, out, counter);
-}
-
-// ---------------------------------------------------------------- cgs_final
-// vout <- w - sum_i coef_i sc_i V_i ;  out = ||vout||^2.  (vout may alias w)
-__global__ void __launch_bounds__(VB) k_cgs_final(int64_t n, int k, const double* __restrict__ V,
-                                                  int64_t ldv, const double* w,
-                                                  const double* __restrict__ sc,
-                                                  const double* __restrict__ coef, double* vout,
-                                                  double* partial, double* out,
-                                                  unsigned* counter) {
-  __shared__ double cf[kMaxRestart + 1];
-  for (int i = threadIdx.x; i < k; i += VB) cf[i] = coef ? coef[i] * sc[i] : 0.0;
-  __syncthreads();
-  double acc = 0.0;
-  const int64_t nsub = (n + SUB - 1) / SUB;
-  for (int64_t s = blockIdx.x; s < nsub; s += gridDim.x) {
-    const int64_t e = s * SUB + threadIdx.x;
-    if (e < n) {
-      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-      int i = 0;
-      for (; i + 3 < k; i += 4) {
-        s0 += cf[i] * __ldg(V + (size_t)i * ldv + e);
-        s1 += cf[i + 1] * __ldg(V + (size_t)(i + 1) * ldv + e);
-        s2 += cf[i + 2] * __ldg(V + (size_t)(i + 2) * ldv + e);
-        s3 += cf[i + 3] * __ldg(V + (size_t)(i + 3) * ldv + e);
-      }
-      for (; i < k; ++i) s0 += cf[i] * __ldg(V + (size_t)i * ldv + e);
-      const double v = w[e] - ((s0 + s1) + (s2 + s3));
-      vout[e] = v;
-      acc += v * v;
-    }
-  }
-  const double b = block_sum(acc);
-  if (threadIdx.x == 0) partial[blockIdx.x] = b;
-  last_block_finish(partial, 1, nullptr, out, counter);
-}
-
-// ---------------------------------------------------------------- misc vector kernels
-// out = b - t  (into out), partial ||out||^2 -> res
-__global__ void __launch_bounds__(VB) k_sub_nrm2(int64_t n, const double* __restrict__ b,
-                                                 const double* __restrict__ t, double* out,
-                                                 double* partial, double* res,
-                                                 unsigned* counter) {
-  double acc = 0.0;
-  const int64_t nsub = (n + SUB - 1) / SUB;
-  for (int64_t s = blockIdx.x; s < nsub; s += gridDim.x) {
-    const int64_t e = s * SUB + threadIdx.x;
-    if (e < n) {
-      const double v = b[e] - (t ? t[e] : 0.0);
-      if (out) out[e] = v;
-      acc += v * v;
-    }
-  }
-  const double bs = block_sum(acc);
-  if (threadIdx.x == 0) partial[blockIdx.x] = bs;
-  last_block_finish(partial, 1, nullptr, res, counter);
-}
-
-// x += sum_{i<k} y_i * (sc ? sc_i : 1) * V_i
-__global__ void __launch_bounds__(VB) k_update_x(int64_t n, const GState* st,
-                                                 const double* __restrict__ V, int64_t ldv,
-                                                 bool use_sc, double* __restrict__ x) {
-  __shared__ double cf[kMaxRestart + 1];
-  const int k = st->k;
-  for (int i = threadIdx.x; i < k; i += VB) cf[i] = st->y[i] * (use_sc ? st->sc[i] : 1.0);
-  __syncthreads();
-  for (int64_t e = blockIdx.x * (int64_t)VB + threadIdx.x; e < n; e += (int64_t)gridDim.x * VB) {
-    double s0 = 0.0;
-    for (int i = 0; i < k; ++i) s0 += cf[i] * __ldg(V + (size_t)i * ldv + e);
-    x[e] += s0;
-  }
-}
-
-// y_i <- scale * x_i
-__global__ void k_scale(int64_t n, const double* __restrict__ x, const double* __restrict__ sc,
-                        double* __restrict__ y) {
-  const double s = *sc;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
-       e += (int64_t)gridDim.x * blockDim.x)
-    y[e] = s * x[e];
-}
+namespace {
 
 // ---------------------------------------------------------------- scalar kernels (1 thread)
 __global__ void k_cycle_init(GState* st) {
@@ -312,20 +125,19 @@ __global__ void k_arnoldi_step(GState* st, int j, int m) {
   if (st->est <= st->target || brk || j + 1 == m) st->done = 1;
 }
 
-// Back substitution H(0:k,0:k) y = g(0:k).
+// Back substitution H(0:k,0:k) y = g(0:k), one warp (lanes split the row sums).
 __global__ void k_lsq(GState* st) {
   const int ld = kMaxRestart + 1;
   const int k = st->k;
+  const int lane = threadIdx.x;
   for (int i = k - 1; i >= 0; --i) {
-    double s = st->g[i];
-    for (int q = i + 1; q < k; ++q) s -= st->H[(size_t)q * ld + i] * st->y[q];
-    st->y[i] = s / st->H[(size_t)i * ld + i];
+    double s = 0.0;
+    for (int q = i + 1 + lane; q < k; q += 32) s += st->H[(size_t)q * ld + i] * st->y[q];
+    s = vec::warp_sum(s);
+    if (lane == 0) st->y[i] = (st->g[i] - s) / st->H[(size_t)i * ld + i];
+    __syncwarp();
+    __threadfence_block();
   }
-}
-
-inline int vgrid(int64_t n) {
-  const int64_t nsub = (n + SUB - 1) / SUB;
-  return (int)std::max<int64_t>(1, std::min<int64_t>(nsub, 148 * 8));
 }
 
 }  // namespace
@@ -347,9 +159,14 @@ int Workspace::ensure(int64_t n_, int m_, bool flex_) {
   if (flex) CPM_TRY(al((void**)&Z, sizeof(double) * (size_t)ldv * m));
   CPM_TRY(al((void**)&w, sizeof(double) * (size_t)ldv));
   CPM_TRY(al((void**)&t, sizeof(double) * (size_t)ldv));
-  CPM_TRY(al((void**)&partial, sizeof(double) * (size_t)148 * 8 * (kMaxRestart + 1)));
+  CPM_TRY(al((void**)&partial, sizeof(double) * (size_t)kMaxBlocks * (kMaxRestart + 8)));
   CPM_TRY(al((void**)&st, sizeof(GState)));
+  CPM_TRY(al((void**)&segoff, sizeof(int64_t) * 2));
   CPM_CUDA(cudaMemset(st, 0, sizeof(GState)));
+  int64_t off[2] = {0, n};
+  CPM_CUDA(cudaMemcpy(segoff, off, sizeof(off), cudaMemcpyHostToDevice));
+  const int64_t nsub = (n + vec::VB - 1) / vec::VB;
+  gps = (int)std::max<int64_t>(1, std::min<int64_t>(nsub, 148 * 8));
   if (cudaMallocHost((void**)&hst, sizeof(HostState)) != cudaSuccess)
     return fail(CPM_ERR_NOMEM, "pinned host state allocation failed");
   return CPM_OK;
@@ -362,9 +179,11 @@ void Workspace::release() {
   if (t) cudaFree(t);
   if (partial) cudaFree(partial);
   if (st) cudaFree(st);
+  if (segoff) cudaFree(segoff);
   if (hst) cudaFreeHost(hst);
   V = Z = w = t = partial = nullptr;
   st = nullptr;
+  segoff = nullptr;
   hst = nullptr;
   n = 0;
   m = 0;
@@ -387,16 +206,20 @@ int gmres_device(const LinOp& A, const PrecOp* M, const double* b, double* x, in
   if (!(rtol > 0.0)) return fail(CPM_ERR_ARG, "cpm_solve: rtol must be > 0");
   const bool flex = M != nullptr;
   CPM_TRY(ws.ensure(n, m, flex));
-  const int G = vgrid(n);
+  const vec::Seg S{ws.segoff, 1, ws.gps};
+  const int G = ws.gps;
   GState* st = ws.st;
-  unsigned* cnt = st->counter;  // device address arithmetic on a device pointer
+  unsigned* cnt = st->counter;  // address arithmetic on a device pointer
 
-  // ||b||, target
+  auto allreduce = [&](double* buf, size_t nv) -> int {
+    return A.allreduce ? A.allreduce(buf, nv, s) : CPM_OK;
+  };
   {
     ProfScope ps(K_OTHER, s);
-    k_sub_nrm2<<<G, VB, 0, s>>>(n, b, nullptr, nullptr, ws.partial, &st->beta2, cnt);
+    vec::k_sub_nrm2<<<G, VB, 0, s>>>(S, b, nullptr, nullptr, ws.partial, &st->beta2, 0, cnt);
     count_launch();
   }
+  CPM_TRY(allreduce(&st->beta2, 1));
   CPM_CUDA(cudaMemcpyAsync(&ws.hst->est, &st->beta2, sizeof(double), cudaMemcpyDeviceToHost, s));
   CPM_CUDA(cudaStreamSynchronize(s));
   const double bnorm = sqrt(ws.hst->est);
@@ -415,8 +238,9 @@ int gmres_device(const LinOp& A, const PrecOp* M, const double* b, double* x, in
     CPM_TRY(A.apply(x, ws.t, nullptr, s));
     {
       ProfScope ps(K_AXPY, s);
-      k_sub_nrm2<<<G, VB, 0, s>>>(n, b, ws.t, ws.V, ws.partial, &st->beta2, cnt);
+      vec::k_sub_nrm2<<<G, VB, 0, s>>>(S, b, ws.t, ws.V, ws.partial, &st->beta2, 0, cnt);
       count_launch();
+      CPM_TRY(allreduce(&st->beta2, 1));
       k_cycle_init<<<1, 1, 0, s>>>(st);
       count_launch();
     }
@@ -433,7 +257,7 @@ int gmres_device(const LinOp& A, const PrecOp* M, const double* b, double* x, in
       if (flex) {
         {
           ProfScope ps(K_AXPY, s);
-          k_scale<<<G, VB, 0, s>>>(n, Vj, &st->sc[j], ws.w);
+          vec::k_scale<<<G, VB, 0, s>>>(S, Vj, st->sc, 0, j, ws.w);
           count_launch();
         }
         double* Zj = ws.Z + (size_t)j * ws.ldv;
@@ -445,21 +269,21 @@ int gmres_device(const LinOp& A, const PrecOp* M, const double* b, double* x, in
       const int k = j + 1;
       {
         ProfScope ps(K_MDOT, s);
-        k_mdot<<<G, VB, 0, s>>>(n, k, ws.V, ws.ldv, ws.w, st->sc, ws.partial, st->h1, cnt + 1);
-        count_launch();
+        CPM_TRY(launch_mdot(S, k, ws.V, ws.ldv, ws.w, st->sc, 0, ws.partial, st->h1, 0, cnt + 1, s));
+        CPM_TRY(allreduce(st->h1, k));
       }
       {
         ProfScope ps(K_CGS_UPDATE, s);
-        k_cgs_update<<<G, VB, 0, s>>>(n, k, ws.V, ws.ldv, ws.w, st->sc, st->h1, ws.partial,
-                                      st->h2, cnt + 2);
-        count_launch();
+        CPM_TRY(launch_cgs_update(S, k, ws.V, ws.ldv, ws.w, st->sc, 0, st->h1, ws.partial, st->h2, 0,
+                                  cnt + 2, s));
+        CPM_TRY(allreduce(st->h2, k));
       }
       {
         ProfScope ps(K_CGS_FINAL, s);
-        k_cgs_final<<<G, VB, 0, s>>>(n, k, ws.V, ws.ldv, ws.w, st->sc, st->h2,
-                                     ws.V + (size_t)(j + 1) * ws.ldv, ws.partial, &st->nrm2,
-                                     cnt + 3);
-        count_launch();
+        CPM_TRY(launch_cgs_final(S, k, ws.V, ws.ldv, ws.w, st->sc, 0, st->h2, 0,
+                                 ws.V + (size_t)(j + 1) * ws.ldv, ws.partial, &st->nrm2, 0, cnt + 3,
+                                 s));
+        CPM_TRY(allreduce(&st->nrm2, 1));
       }
       {
         ProfScope ps(K_OTHER, s);
@@ -472,9 +296,10 @@ int gmres_device(const LinOp& A, const PrecOp* M, const double* b, double* x, in
     }
     {
       ProfScope ps(K_AXPY, s);
-      k_lsq<<<1, 1, 0, s>>>(st);
+      k_lsq<<<1, 32, 0, s>>>(st);
       count_launch();
-      k_update_x<<<G, VB, 0, s>>>(n, st, flex ? ws.Z : ws.V, ws.ldv, !flex, x);
+      vec::k_combine<<<G, VB, 0, s>>>(S, flex ? ws.Z : ws.V, ws.ldv, st->y, 0, flex ? nullptr : st->sc, 0,
+                                      &st->k, 0, 0, nullptr, nullptr, nullptr, x, 1);
       count_launch();
     }
     CPM_CUDA(cudaGetLastError());
@@ -488,15 +313,15 @@ int gmres_device(const LinOp& A, const PrecOp* M, const double* b, double* x, in
     }
     if (its >= maxit) break;
   }
-  // true residual
   double rtrue = 0.0;
   if (stats) {
     CPM_TRY(A.apply(x, ws.t, nullptr, s));
     {
       ProfScope ps(K_OTHER, s);
-      k_sub_nrm2<<<G, VB, 0, s>>>(n, b, ws.t, nullptr, ws.partial, &st->beta2, cnt);
+      vec::k_sub_nrm2<<<G, VB, 0, s>>>(S, b, ws.t, nullptr, ws.partial, &st->beta2, 0, cnt);
       count_launch();
     }
+    CPM_TRY(allreduce(&st->beta2, 1));
     CPM_CUDA(cudaMemcpyAsync(&ws.hst->est, &st->beta2, sizeof(double), cudaMemcpyDeviceToHost, s));
     CPM_CUDA(cudaStreamSynchronize(s));
     rtrue = sqrt(ws.hst->est);
@@ -507,19 +332,9 @@ int gmres_device(const LinOp& A, const PrecOp* M, const double* b, double* x, in
     stats->resid_est = est;
     stats->resid_true = rtrue;
     stats->bnorm = bnorm;
-    stats->seconds =
-        std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    stats->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   }
   CPM_CUDA(cudaStreamSynchronize(s));
-  return CPM_OK;
-}
-
-// Exposed helpers for the RAS local solver / tests.
-int vec_nrm2(const double* x, int64_t n, double* d_out, Workspace& ws, cudaStream_t s) {
-  const int G = vgrid(n);
-  k_sub_nrm2<<<G, VB, 0, s>>>(n, x, nullptr, nullptr, ws.partial, d_out, ws.st->counter);
-  count_launch();
-  CPM_CUDA(cudaGetLastError());
   return CPM_OK;
 }
 

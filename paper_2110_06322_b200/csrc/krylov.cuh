@@ -11,6 +11,7 @@
 namespace cpm {
 
 constexpr int kMaxRestart = 128;
+constexpr int kMaxBlocks = 4096;  // max grid of a segmented vector kernel
 
 // Device-resident Arnoldi / Givens state of one (F)GMRES solve.
 struct GState {
@@ -18,7 +19,7 @@ struct GState {
   double cs[kMaxRestart], sn[kMaxRestart];
   double g[kMaxRestart + 1], y[kMaxRestart];
   double sc[kMaxRestart + 1];                 // 1/||w_i|| of the stored basis vectors
-  double h1[kMaxRestart + 1], h2[kMaxRestart + 1];
+  double h1[kMaxRestart + 2], h2[kMaxRestart + 2];
   double nrm2, beta, target;
   int k, done, breakdown, its;                // contiguous: copied to the host together
   double est, beta2;                          // contiguous
@@ -33,6 +34,8 @@ struct HostState {
 // y = scale * A x  (scale: device pointer or nullptr)
 struct LinOp {
   std::function<int(const double*, double*, const double*, cudaStream_t)> apply;
+  // sum-allreduce of n device doubles across ranks (empty on one GPU)
+  std::function<int(double*, size_t, cudaStream_t)> allreduce;
 };
 // z = M r
 struct PrecOp {
@@ -48,6 +51,8 @@ struct Workspace {
   double* w = nullptr;
   double* t = nullptr;
   double* partial = nullptr;
+  int64_t* segoff = nullptr;       // {0, n}
+  int gps = 1;                     // blocks per segment
   GState* st = nullptr;
   HostState* hst = nullptr;
   int ensure(int64_t n, int m, bool flex);

@@ -21,7 +21,7 @@ extern "C" int cpm_solve(const cpm_band* b, double c, const double* f, double* u
   cudaStream_t s = (cudaStream_t)stream;
   LinOp A;
   A.apply = [b, c](const double* x, double* y, const double* scale, cudaStream_t st) {
-    return apply_device(b, c, x, y, scale, st);
+    return apply_device(b, c, x, y, scale, 0, st);
   };
   PrecOp M;
   if (ras) {

@@ -1,0 +1,271 @@
+// vecops.cuh — segmented, deterministic Krylov vector kernels (private).
+//
+// A "segmented" vector is the concatenation of nseg independent vectors
+// (segment s = elements [off[s], off[s+1])).  The global GMRES uses one segment;
+// the RAS preconditioner runs all subdomain GMRES solves as segments of one
+// batched vector.  Grid = nseg * gps blocks; block b works on segment b / gps and
+// visits the segment's elements lb*VB + t, lb*VB + t + gps*VB, ... (lb = b % gps),
+// so every reduction has a fixed association order: per-thread accumulation in
+// element order, warp shuffle tree, warps in index order, blocks in index order
+// (summed by the last block of the segment to finish; threadfence + counter).
+//
+// Basis vectors V_i are stored unnormalised; sc[s*lds + i] = 1/||V_i|| of
+// segment s is applied on the fly.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "internal.cuh"
+
+namespace cpm {
+namespace vec {
+
+constexpr int VB = 256;
+
+struct Seg {
+  const int64_t* off;  // device, nseg + 1
+  int nseg;
+  int gps;             // blocks per segment
+};
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Reduce acc[0..k) over the block into partial[blockIdx.x * pld + i]; then the
+// last block of the segment writes out[s*ldo + i] = scale_i * sum_b partial.
+template <int KMAX>
+__device__ __forceinline__ void block_then_segment_reduce(const double (&acc)[KMAX], int k,
+                                                          double* partial, int pld, int s,
+                                                          int gps, const double* sc, int lds,
+                                                          double* out, int ldo,
+                                                          unsigned* counters) {
+  __shared__ double red[VB / 32][KMAX];
+  __shared__ bool last;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+  for (int i = 0; i < KMAX; ++i) {
+    if (i < k) {
+      const double v = warp_sum(acc[i]);
+      if (lane == 0) red[warp][i] = v;
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < k; i += VB) {
+    double t = 0.0;
+#pragma unroll
+    for (int w = 0; w < VB / 32; ++w) t += red[w][i];
+    partial[(size_t)blockIdx.x * pld + i] = t;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = (atomicAdd(counters + s, 1u) == (unsigned)gps - 1u);
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  for (int i = warp; i < k; i += VB / 32) {
+    double a = 0.0;
+    for (int b = lane; b < gps; b += 32) a += __ldcg(partial + (size_t)(s * gps + b) * pld + i);
+    a = warp_sum(a);
+    if (lane == 0) out[(size_t)s * ldo + i] = sc ? a * sc[(size_t)s * lds + i] : a;
+  }
+  if (threadIdx.x == 0) counters[s] = 0u;
+}
+
+// out_i = sc_i <V_i, w>  (per segment).  Vectors in groups of 8: per group each
+// thread streams its elements with 8 independent loads per element (w re-read
+// from L1/L2 per group), so only 8 accumulators live in registers and
+// occupancy stays high; one block reduction per group.
+static __global__ void __launch_bounds__(VB) k_mdot8(Seg S, int k, const double* __restrict__ V,
+                                              int64_t ldv, const double* __restrict__ w,
+                                              const double* __restrict__ sc, int lds,
+                                              double* partial, int pld, double* out, int ldo,
+                                              unsigned* counters) {
+  const int s = blockIdx.x / S.gps, lb = blockIdx.x % S.gps;
+  const int64_t o0 = S.off[s], n = S.off[s + 1] - o0;
+  __shared__ double red[VB / 32][8];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int g = 0; g < k; g += 8) {
+    const int kg = k - g < 8 ? k - g : 8;
+    double acc[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc[q] = 0.0;
+    const double* Vg = V + (size_t)g * ldv + o0;
+    for (int64_t e = (int64_t)lb * VB + threadIdx.x; e < n; e += (int64_t)S.gps * VB) {
+      const double wv = __ldg(w + o0 + e);
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (q < kg) acc[q] += __ldcs(Vg + (size_t)q * ldv + e) * wv;
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const double v = warp_sum(acc[q]);
+      if (lane == 0) red[warp][q] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < kg) {
+      double t = 0.0;
+#pragma unroll
+      for (int ww = 0; ww < VB / 32; ++ww) t += red[ww][threadIdx.x];
+      partial[(size_t)blockIdx.x * pld + g + threadIdx.x] = t;
+    }
+    __syncthreads();
+  }
+  __shared__ bool last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = (atomicAdd(counters + s, 1u) == (unsigned)S.gps - 1u);
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  for (int i = warp; i < k; i += VB / 32) {
+    double a = 0.0;
+    for (int b = lane; b < S.gps; b += 32) a += __ldcg(partial + (size_t)(s * S.gps + b) * pld + i);
+    a = warp_sum(a);
+    if (lane == 0) out[(size_t)s * ldo + i] = sc ? a * sc[(size_t)s * lds + i] : a;
+  }
+  if (threadIdx.x == 0) counters[s] = 0u;
+}
+
+// w <- w - sum_i coef_i sc_i V_i ;  out_i = sc_i <V_i, w_new>   (per segment)
+template <int KMAX>
+static __global__ void __launch_bounds__(VB) k_cgs_update(Seg S, int k, const double* __restrict__ V,
+                                                   int64_t ldv, double* __restrict__ w,
+                                                   const double* __restrict__ sc, int lds,
+                                                   const double* __restrict__ coef, double* partial,
+                                                   double* out, int ldo, unsigned* counters) {
+  const int s = blockIdx.x / S.gps, lb = blockIdx.x % S.gps;
+  const int64_t o0 = S.off[s], n = S.off[s + 1] - o0;
+  __shared__ double cf[KMAX];
+  for (int i = threadIdx.x; i < k; i += VB) cf[i] = coef[(size_t)s * ldo + i] * sc[(size_t)s * lds + i];
+  __syncthreads();
+  double acc[KMAX];
+#pragma unroll
+  for (int i = 0; i < KMAX; ++i) acc[i] = 0.0;
+  for (int64_t e = (int64_t)lb * VB + threadIdx.x; e < n; e += (int64_t)S.gps * VB) {
+    const double* p = V + o0 + e;
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+    for (int i = 0; i < KMAX; i += 4) {
+      if (i < k) s0 += cf[i] * __ldg(p + (size_t)i * ldv);
+      if (i + 1 < k) s1 += cf[i + 1] * __ldg(p + (size_t)(i + 1) * ldv);
+      if (i + 2 < k) s2 += cf[i + 2] * __ldg(p + (size_t)(i + 2) * ldv);
+      if (i + 3 < k) s3 += cf[i + 3] * __ldg(p + (size_t)(i + 3) * ldv);
+    }
+    const double wv = w[o0 + e] - ((s0 + s1) + (s2 + s3));
+    w[o0 + e] = wv;
+#pragma unroll
+    for (int i = 0; i < KMAX; ++i)
+      if (i < k) acc[i] += __ldg(p + (size_t)i * ldv) * wv;   // L1/L2 re-read
+  }
+  block_then_segment_reduce<KMAX>(acc, k, partial, KMAX, s, S.gps, sc, lds, out, ldo, counters);
+}
+
+// vout <- w - sum_i coef_i sc_i V_i ; out = ||vout||^2 (per segment). vout may alias w.
+static __global__ void __launch_bounds__(VB) k_cgs_final(Seg S, int k, const double* __restrict__ V,
+                                                  int64_t ldv, const double* w,
+                                                  const double* __restrict__ sc, int lds,
+                                                  const double* __restrict__ coef, int ldo,
+                                                  double* vout, double* partial, double* out,
+                                                  int ldn, unsigned* counters) {
+  const int s = blockIdx.x / S.gps, lb = blockIdx.x % S.gps;
+  const int64_t o0 = S.off[s], n = S.off[s + 1] - o0;
+  __shared__ double cf[132];
+  for (int i = threadIdx.x; i < k; i += VB) cf[i] = coef[(size_t)s * ldo + i] * sc[(size_t)s * lds + i];
+  __syncthreads();
+  double acc[1] = {0.0};
+  for (int64_t e = (int64_t)lb * VB + threadIdx.x; e < n; e += (int64_t)S.gps * VB) {
+    const double* p = V + o0 + e;
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    int i = 0;
+    for (; i + 3 < k; i += 4) {
+      s0 += cf[i] * __ldcs(p + (size_t)i * ldv);
+      s1 += cf[i + 1] * __ldcs(p + (size_t)(i + 1) * ldv);
+      s2 += cf[i + 2] * __ldcs(p + (size_t)(i + 2) * ldv);
+      s3 += cf[i + 3] * __ldcs(p + (size_t)(i + 3) * ldv);
+    }
+    for (; i < k; ++i) s0 += cf[i] * __ldcs(p + (size_t)i * ldv);
+    const double v = w[o0 + e] - ((s0 + s1) + (s2 + s3));
+    vout[o0 + e] = v;
+    acc[0] += v * v;
+  }
+  block_then_segment_reduce<1>(acc, 1, partial, 1, s, S.gps, nullptr, 0, out, ldn, counters);
+}
+
+// out = b - t (t may be null), ||out||^2 per segment into res[s*ldr]. out may be null.
+static __global__ void __launch_bounds__(VB) k_sub_nrm2(Seg S, const double* __restrict__ b,
+                                                 const double* __restrict__ t, double* out,
+                                                 double* partial, double* res, int ldr,
+                                                 unsigned* counters) {
+  const int s = blockIdx.x / S.gps, lb = blockIdx.x % S.gps;
+  const int64_t o0 = S.off[s], n = S.off[s + 1] - o0;
+  double acc[1] = {0.0};
+  for (int64_t e = (int64_t)lb * VB + threadIdx.x; e < n; e += (int64_t)S.gps * VB) {
+    const double v = b[o0 + e] - (t ? t[o0 + e] : 0.0);
+    if (out) out[o0 + e] = v;
+    acc[0] += v * v;
+  }
+  block_then_segment_reduce<1>(acc, 1, partial, 1, s, S.gps, nullptr, 0, res, ldr, counters);
+}
+
+// x[dst] += sum_{i<k_s} y_si * sc_si * V_i[src]  over a per-segment element range
+// [lo_s, hi_s) of V (src = o0 + lo + q) written to xo[xoff_s + q].
+// coefs: y at ys[s*ldy + i], sc at sc[s*lds + i] (sc may be null), k_s at ks[s] or k.
+static __global__ void __launch_bounds__(VB) k_combine(Seg S, const double* __restrict__ V, int64_t ldv,
+                                                const double* __restrict__ ys, int ldy,
+                                                const double* __restrict__ sc, int lds,
+                                                const int* ks, int ks_ld, int kfix,
+                                                const int64_t* lo, const int64_t* hi,
+                                                const int64_t* xoff, double* __restrict__ x,
+                                                int accumulate) {
+  const int s = blockIdx.x / S.gps, lb = blockIdx.x % S.gps;
+  const int64_t o0 = S.off[s];
+  const int64_t a = lo ? lo[s] : 0, bnd = hi ? hi[s] : (S.off[s + 1] - o0);
+  const int64_t xo = xoff ? xoff[s] : o0;
+  const int k = ks ? ks[(size_t)s * ks_ld] : kfix;
+  __shared__ double cf[130];
+  for (int i = threadIdx.x; i < k; i += VB)
+    cf[i] = ys[(size_t)s * ldy + i] * (sc ? sc[(size_t)s * lds + i] : 1.0);
+  __syncthreads();
+  for (int64_t q = a + (int64_t)lb * VB + threadIdx.x; q < bnd; q += (int64_t)S.gps * VB) {
+    const double* p = V + o0 + q;
+    double s0 = 0.0, s1 = 0.0;
+    int i = 0;
+    for (; i + 1 < k; i += 2) {
+      s0 += cf[i] * __ldg(p + (size_t)i * ldv);
+      s1 += cf[i + 1] * __ldg(p + (size_t)(i + 1) * ldv);
+    }
+    if (i < k) s0 += cf[i] * __ldg(p + (size_t)i * ldv);
+    const int64_t d = xo + (q - a);
+    x[d] = (accumulate ? x[d] : 0.0) + (s0 + s1);
+  }
+}
+
+// y = sc_s[idx] * x per segment (scale pointer per segment: sc[s*lds + idx])
+static __global__ void __launch_bounds__(VB) k_scale(Seg S, const double* __restrict__ x,
+                                              const double* __restrict__ sc, int lds, int idx,
+                                              double* __restrict__ y) {
+  const int s = blockIdx.x / S.gps, lb = blockIdx.x % S.gps;
+  const int64_t o0 = S.off[s], n = S.off[s + 1] - o0;
+  const double f = sc[(size_t)s * lds + idx];
+  for (int64_t e = (int64_t)lb * VB + threadIdx.x; e < n; e += (int64_t)S.gps * VB)
+    y[o0 + e] = f * x[o0 + e];
+}
+
+}  // namespace vec
+
+// Launch helpers choosing the register-array width from k.
+int launch_mdot(const vec::Seg& S, int k, const double* V, int64_t ldv, const double* w,
+                const double* sc, int lds, double* partial, double* out, int ldo,
+                unsigned* counters, cudaStream_t st);  // k <= kMaxRestart + 2
+int launch_cgs_update(const vec::Seg& S, int k, const double* V, int64_t ldv, double* w,
+                      const double* sc, int lds, const double* coef, double* partial, double* out,
+                      int ldo, unsigned* counters, cudaStream_t st);
+int launch_cgs_final(const vec::Seg& S, int k, const double* V, int64_t ldv, const double* w,
+                     const double* sc, int lds, const double* coef, int ldo, double* vout,
+                     double* partial, double* out, int ldn, unsigned* counters, cudaStream_t st);
+
+}  // namespace cpm

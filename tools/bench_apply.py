@@ -1,0 +1,48 @@
+"""Quick apply / GMRES-kernel timing on config 1 (for iterating on kernels)."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+
+import paper_2110_06322_b200 as cpm
+import seeded_inputs
+
+h = float(os.environ.get("CPM_H", 1.0 / 200))
+band = cpm.cpm_build_band("sphere", h)
+coords = cpm.cpm_band_active_coords(band).astype(np.int64)
+u = torch.from_numpy(seeded_inputs.uniform_pm1(0, coords)).cuda()
+y = torch.empty_like(u)
+for _ in range(5):
+    cpm.cpm_apply(band, 10.0, u, y)
+torch.cuda.synchronize()
+cpm.cpm_profile_reset()
+cpm.cpm_profile_enable(True)
+N = 50
+a = torch.cuda.Event(enable_timing=True)
+b = torch.cuda.Event(enable_timing=True)
+a.record()
+for _ in range(N):
+    cpm.cpm_apply(band, 10.0, u, y)
+b.record()
+torch.cuda.synchronize()
+cpm.cpm_profile_enable(False)
+ms = a.elapsed_time(b) / N
+e, _ = cpm.cpm_profile_read("extend")
+l, _ = cpm.cpm_profile_read("laplace")
+nA, nG = band.info.n_active, band.info.n_ghost
+alg = 16 * nA + 28 * (nA + nG)
+print(f"nA={nA} tiles={band.info.n_tiles} maxbox={band.info.max_box} apply {ms*1e3:.1f} us "
+      f"(extend {e/N*1e3:.1f} us, laplace {l/N*1e3:.1f} us) -> {alg/ms/1e6:.0f} GB/s alg, "
+      f"{nA/ms/1e6:.2f} Gnodes/s")
+if os.environ.get("CPM_SOLVE"):
+    f = torch.empty_like(u)
+    cpm.cpm_eval_sph(band, 6, 3, 52.0, f)
+    x = torch.zeros_like(u)
+    cpm.cpm_profile_reset()
+    cpm.cpm_profile_enable(True)
+    st = cpm.cpm_solve(band, 10.0, f, x, rtol=1e-10, restart=50, maxit=200)
+    cpm.cpm_profile_enable(False)
+    out = {k: cpm.cpm_profile_read(k) for k in ["extend", "laplace", "mdot", "cgs_update", "cgs_final", "axpy", "other"]}
+    print("solve 200 its:", f"{st.seconds:.3f}s", {k: f"{v[0]:.1f}ms/{v[1]}" for k, v in out.items()})
