@@ -3,16 +3,23 @@
 //   y = c u - [Delta_h E u - (6/h^2)(u - E u)]          (Eq. 4, d = 3)
 //     = (c + 6/h^2) u - (1/h^2) sum_{6 nbrs j} (E u)_j    (the centre (E u)_i terms cancel)
 //
-// Two kernels per apply, one CTA per tile (= occupied 8^3 brick):
-//   extend  : stage the tile's 4x4x4-stencil box of u in shared memory (fill
-//             runs of consecutive band-order sources), then for every eval node
-//             (Sigma_A u Sigma_G in the brick) recompute the tricubic Lagrange
-//             weights from its fractional offsets and contract
-//             x, then y, then z.  E u is written to a dense per-brick scratch vb.
-//   laplace : for every output node, 6 neighbour reads of vb (same brick or a
-//             face-neighbour brick) and the diagonal term.
+// Two kernels per apply:
+//   k_extend  (persistent, one tile = occupied 8^3 brick at a time per CTA):
+//             stage the cells of u the tile's stencils read into a shared-memory
+//             box (fill runs of consecutive band-order sources, 8 lanes per run,
+//             cp.async), prefetching the next tile's box and node offsets while the
+//             current tile is contracted; for every eval node (Sigma_A u Sigma_G in
+//             the brick) recompute the tricubic Lagrange weights from its fractional
+//             offsets and contract x, then y, then z.  Nodes of a tile
+//             are sorted by stencil base, so the lanes of a warp read overlapping
+//             stencils (shared-memory broadcast).  E u goes to the tile's compact
+//             slot range of vb (cell order, TileHdr::emask ranks).
+//   k_laplace (one CTA per tile): gather the tile's E u and the face layers of its
+//             6 neighbour tiles into a dense 10^3 halo brick in shared memory, then
+//             the 7-point combination for every output node.
 // HBM-bound by design (no tensor cores: this is a gather, not a dense
-// contraction).  Bytes per apply: DESIGN.md §"Roofline".
+// contraction).  Node offsets are streamed with evict-first loads so that u and
+// vb stay resident in the 126 MB L2 between the two kernels.
 #include <algorithm>
 
 #include "internal.cuh"
@@ -20,14 +27,18 @@
 namespace cpm {
 namespace {
 
-// Degree-3 Lagrange weights on nodes (-1, 0, 1, 2) at t (product form).
+// Degree-3 Lagrange weights on nodes (-1, 0, 1, 2) at t (reading R2),
+// factored through q = t(t-1) and p = (t+1)(t-2)/2 = q/2 - 1:
+//   w0 = -t(t-1)(t-2)/6 = q(2-t)/6    w1 = (t+1)(t-1)(t-2)/2 = p(t-1)
+//   w2 = -(t+1)t(t-2)/2 = -p t        w3 = (t+1)t(t-1)/6 = q(t+1)/6
 __device__ __forceinline__ void lagrange4(double t, double w[4]) {
-  const double a = t + 1.0, c = t - 1.0, d = t - 2.0;
-  const double cd = c * d, at = a * t;
-  w[0] = -(t * cd) * (1.0 / 6.0);
-  w[1] = (a * cd) * 0.5;
-  w[2] = -(at * d) * 0.5;
-  w[3] = (at * c) * (1.0 / 6.0);
+  const double q = fma(t, t, -t);
+  const double q6 = q * (1.0 / 6.0), q3 = q * (1.0 / 3.0);
+  const double p = fma(q, 0.5, -1.0);
+  w[0] = fma(-q6, t, q3);
+  w[1] = fma(p, t, -p);
+  w[2] = -p * t;
+  w[3] = fma(q6, t, q6);
 }
 
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
@@ -44,165 +55,199 @@ __device__ __forceinline__ void cp_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
-constexpr int kExtThreads = 256;
-constexpr int kExtMinBlocks = 4;   // CTAs per SM the register budget is sized for
-constexpr int kNodesPerThread = 2; // eval nodes per tile <= 512 = 2 * kExtThreads
+// ------------------------------------------------------------------ node-per-thread extend
+// One CTA (128 threads) per tile, up to 4 eval nodes per thread, 8 CTAs per SM:
+//   1. streaming loads of the tile's node offsets into registers (evict-first)
+//   2. cp.async of the run descriptors into shared memory
+//   3. cp.async of the box cells, 8 lanes per run (one coalesced 64-byte read)
+//   4. per node: Lagrange weights from the offsets, x-y-z contraction -> vb
+// The tile's nodes are sorted by stencil base, so the lanes of a half-warp read
+// few distinct addresses (broadcast).  u is read with an evict-last L2 policy
+// and vb written with one, so both stay resident in L2 for k_laplace.
+constexpr int kNtThreads = 128;
+constexpr int kNtNodes = 4;  // eval nodes per tile <= 512 = 4 * kNtThreads
 
-// Issue the asynchronous copies of tile t's stencil box (fill runs, 8 lanes per
-// run; cp.async = LDGSTS).  ZERO: clear the box first.
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void cp_async8_hint(void* smem, const void* gmem, uint64_t pol) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem),
+               "l"(pol));
+}
+__device__ __forceinline__ double ld_hint(const double* p, uint64_t pol) {
+  double v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;\n"
+               : "=d"(v)
+               : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ uint32_t ld_hint(const uint32_t* p, uint64_t pol) {
+  uint32_t v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;\n"
+               : "=r"(v)
+               : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ void st_hint(double* p, double v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;\n" ::"l"(p), "d"(v), "l"(pol) : "memory");
+}
+
 template <bool ZERO>
-__device__ __forceinline__ void stage_box(const TileHdr* __restrict__ tiles,
-                                          const uint64_t* __restrict__ runs,
-                                          const double* __restrict__ u,
-                                          const double* __restrict__ uh, uint32_t split, int t,
-                                          double* box) {
+__global__ void __launch_bounds__(kNtThreads, 8)
+    k_extend_nt(const TileHdr* __restrict__ tiles, int boxCells, int descCap,
+                const uint64_t* __restrict__ runs, const double* __restrict__ u,
+                const double* __restrict__ uh, uint32_t split, const double* __restrict__ tx,
+                const double* __restrict__ ty, const double* __restrict__ tz,
+                const uint32_t* __restrict__ eoff, double* __restrict__ vb) {
+  extern __shared__ double smn[];
+  double* box = smn;
+  uint64_t* desc = (uint64_t*)(box + boxCells);
+  const int t = blockIdx.x, tid = threadIdx.x;
   const TileHdr* T = tiles + t;
-  const int r0 = T->r0, r1 = T->r1;
-  if (ZERO) {
-    const int nbox = T->pad[1] * T->sz;
-    for (int c = threadIdx.x; c < nbox; c += kExtThreads) box[c] = 0.0;
-    __syncthreads();
-  }
-  // Thread-per-run: all run descriptors of the tile are loaded up front (4 per
-  // thread in flight), then each thread issues the LDGSTS copies of its runs.
-  // (A dependent descriptor->copy chain per loop trip was the kernel's main stall.)
-  const int nr = r1 - r0;
-  for (int base = 0; base < nr; base += 4 * kExtThreads) {
-    uint64_t d[4];
+  const int e0 = T->e0, ne = T->e1 - e0, r0 = T->r0, r1 = T->r1;
+  const int sx = T->pad[0], sxy = T->pad[1];
+  const uint64_t pfirst = policy_evict_first(), plast = policy_evict_last();
+  double nt[kNtNodes][3];
+  uint32_t eo[kNtNodes];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int r = base + threadIdx.x + k * kExtThreads;
-      d[k] = r < nr ? __ldg(runs + r0 + r) : 0ull;
-    }
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const uint32_t src = (uint32_t)d[k], dst = (uint32_t)(d[k] >> 32) & 0xffffu,
-                     len = (uint32_t)(d[k] >> 48) & 0xffu;
-      const double* gsrc = src >= split ? uh + (src - split) : u + src;  // runs never straddle split
-      for (uint32_t q = 0; q < len; ++q) cp_async8(box + dst + q, gsrc + q);
-    }
-  }
-}
-
-struct NodeRegs {
-  double t[kNodesPerThread][3];
-  uint32_t eo[kNodesPerThread];
-  int n;
-};
-
-__device__ __forceinline__ void load_nodes(const TileHdr* __restrict__ tiles,
-                                           const double* __restrict__ tx,
-                                           const double* __restrict__ ty,
-                                           const double* __restrict__ tz,
-                                           const uint32_t* __restrict__ eoff, int t, NodeRegs& R) {
-  const int e0 = tiles[t].e0, ne = tiles[t].e1 - e0;
-  R.n = ne;
-#pragma unroll
-  for (int k = 0; k < kNodesPerThread; ++k) {
-    const int i = threadIdx.x + k * kExtThreads;
+  for (int k = 0; k < kNtNodes; ++k) {
+    const int i = tid + k * kNtThreads;
     if (i < ne) {
-      R.t[k][0] = __ldg(tx + e0 + i);
-      R.t[k][1] = __ldg(ty + e0 + i);
-      R.t[k][2] = __ldg(tz + e0 + i);
-      R.eo[k] = __ldg(eoff + e0 + i);
+      nt[k][0] = ld_hint(tx + e0 + i, pfirst);
+      nt[k][1] = ld_hint(ty + e0 + i, pfirst);
+      nt[k][2] = ld_hint(tz + e0 + i, pfirst);
+      eo[k] = ld_hint(eoff + e0 + i, pfirst);
     }
   }
-}
-
-// Persistent extend: CTA b handles tiles b, b + G, b + 2G, ...  While tile t is
-// contracted, tile t + G's stencil box streams into the other shared-memory
-// buffer (cp.async) and its node offsets into registers, so the global-memory
-// latency of one tile overlaps the FP64 / shared-memory work of the previous.
-template <bool ZERO>
-__global__ void __launch_bounds__(kExtThreads, kExtMinBlocks)
-    k_extend(const TileHdr* __restrict__ tiles, int nT, int boxCells,
-             const uint64_t* __restrict__ runs, const double* __restrict__ u,
-             const double* __restrict__ uh, uint32_t split,
-             const double* __restrict__ tx, const double* __restrict__ ty,
-             const double* __restrict__ tz, const uint32_t* __restrict__ eoff,
-             double* __restrict__ vb) {
-  extern __shared__ double smem[];
-  int t = blockIdx.x;
-  if (t >= nT) return;
-  NodeRegs cur, nxt;
-  stage_box<ZERO>(tiles, runs, u, uh, split, t, smem);
-  cp_commit();
-  load_nodes(tiles, tx, ty, tz, eoff, t, cur);
-  int b = 0;
-  for (; t < nT; t += gridDim.x) {
-    const int tn = t + gridDim.x;
-    if (tn < nT) {
-      stage_box<ZERO>(tiles, runs, u, uh, split, tn, smem + (size_t)(b ^ 1) * boxCells);
-      load_nodes(tiles, tx, ty, tz, eoff, tn, nxt);
-    }
+  if (ZERO) {
+    const int nbox = sxy * T->sz;
+    for (int c = tid; c < nbox; c += kNtThreads) box[c] = 0.0;
+  }
+  const int g = tid >> 3, l = tid & 7;
+  for (int c0 = r0; c0 < r1; c0 += descCap) {
+    const int nr = min(descCap, r1 - c0);
+    __syncthreads();  // previous round's descriptors consumed (and ZERO clear done)
+    for (int r = tid; r < nr; r += kNtThreads) cp_async8_hint(desc + r, runs + c0 + r, pfirst);
     cp_commit();
-    cp_wait<1>();
+    cp_wait<0>();
     __syncthreads();
-    const double* box = smem + (size_t)b * boxCells;
-    const TileHdr* T = tiles + t;
-    const int sx = T->pad[0], sxy = T->pad[1];
-    double* out = vb + (size_t)t * kBrickCells;
-#pragma unroll
-    for (int k = 0; k < kNodesPerThread; ++k) {
-      if (threadIdx.x + k * kExtThreads < cur.n) {
-        double wx[4], wy[4], wz[4];
-        lagrange4(cur.t[k][0], wx);
-        lagrange4(cur.t[k][1], wy);
-        lagrange4(cur.t[k][2], wz);
-        const uint32_t eo = cur.eo[k];
-        const double* p = box + (eo & 0xffffu);
-        double acc = 0.0;
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          double accy = 0.0;
-#pragma unroll
-          for (int bb = 0; bb < 4; ++bb) {
-            const double* row = p + bb * sx + c * sxy;
-            const double rx = wx[0] * row[0] + wx[1] * row[1] + wx[2] * row[2] + wx[3] * row[3];
-            accy += wy[bb] * rx;
-          }
-          acc += wz[c] * accy;
-        }
-        out[eo >> 16] = acc;
+    for (int r = g; r < nr; r += kNtThreads / 8) {
+      const uint64_t d = desc[r];
+      const uint32_t src = (uint32_t)d, dst = (uint32_t)(d >> 32) & 0xffffu,
+                     len = (uint32_t)(d >> 48) & 0xffu;
+      if (l < len) {
+        const double* gsrc = src >= split ? uh + (src - split) : u + src;  // runs never straddle split
+        cp_async8_hint(box + dst + l, gsrc + l, plast);
       }
     }
-    __syncthreads();  // buffer b is refilled by the next iteration's prefetch
-    cur = nxt;
-    b ^= 1;
+    cp_commit();
   }
   cp_wait<0>();
+  __syncthreads();
+  double* out = vb + (size_t)t * kBrickCells;
+#pragma unroll
+  for (int k = 0; k < kNtNodes; ++k) {
+    if (tid + k * kNtThreads < ne) {
+      double wx[4], wy[4], wz[4];
+      lagrange4(nt[k][0], wx);
+      lagrange4(nt[k][1], wy);
+      lagrange4(nt[k][2], wz);
+      const double* p = box + (eo[k] & 0xffffu);
+      double acc = 0.0;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        double accy = 0.0;
+#pragma unroll
+        for (int bb = 0; bb < 4; ++bb) {
+          const double* row = p + bb * sx + c * sxy;
+          const double rx = (wx[0] * row[0] + wx[1] * row[1]) + (wx[2] * row[2] + wx[3] * row[3]);
+          accy += wy[bb] * rx;
+        }
+        acc += wz[c] * accy;
+      }
+      st_hint(out + (eo[k] >> 16), acc, plast);
+    }
+  }
 }
 
-__global__ void __launch_bounds__(256) k_laplace(const TileHdr* __restrict__ tiles,
-                                                 const double* __restrict__ u,
-                                                 const uint16_t* __restrict__ acell,
-                                                 const double* __restrict__ vb,
-                                                 double* __restrict__ y, double diag, double ih2,
-                                                 const double* __restrict__ scale, int lds) {
-  const int t = blockIdx.x;
+// Dense halo brick: cell (x, y, z), x, y, z in -1..8, at (x+1) + 10 (y+1) + 100 (z+1).
+__device__ __forceinline__ int hidx(int x, int y, int z) { return (x + 1) + 10 * (y + 1) + 100 * (z + 1); }
+
+constexpr int kLapThreads = 256;
+
+// One CTA per tile.  All global loads (own E u, the neighbours' face layers, the
+// output nodes' u and cells) are issued before the single barrier, so a CTA has
+// one dependent chain: header -> neighbour header -> vb.
+__global__ void __launch_bounds__(kLapThreads) k_laplace(const TileHdr* __restrict__ tiles,
+                                                         const double* __restrict__ u,
+                                                         const uint16_t* __restrict__ acell,
+                                                         const double* __restrict__ vb,
+                                                         double* __restrict__ y, double diag,
+                                                         double ih2,
+                                                         const double* __restrict__ scale, int lds) {
+  __shared__ double E[1000];
+  const int t = blockIdx.x, tid = threadIdx.x;
   const TileHdr* T = tiles + t;
   const int a0 = T->a0, a1 = T->a1;
   if (a0 == a1) return;
-  const int n0 = T->nbr[0], n1 = T->nbr[1], n2 = T->nbr[2], n3 = T->nbr[3], n4 = T->nbr[4],
-            n5 = T->nbr[5];
-  const double* vt = vb + (size_t)t * kBrickCells;
+  // output nodes: up to 2 per thread
+  int ac[2];
+  double au[2];
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const int a = a0 + tid + k * kLapThreads;
+    if (a < a1) {
+      ac[k] = __ldg(acell + a);
+      au[k] = __ldg(u + a);
+    }
+  }
+  // 512 own cells + 6 x 64 face cells of the neighbours: 3.5 per thread
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int q = tid + k * kLapThreads;
+    int src = -1, c = 0, h = 0;
+    if (q < kBrickCells) {
+      src = t;
+      c = q;
+      h = hidx(q & 7, (q >> 3) & 7, q >> 6);
+    } else if (q < kBrickCells + 384) {
+      const int f = (q - kBrickCells) >> 6, i = q & 7, j = (q >> 3) & 7;
+      src = T->nbr[f];
+      const int axis = f >> 1, plus = (f & 1) == 0;
+      const int in = plus ? 0 : 7;    // layer read in the neighbour
+      const int out = plus ? 8 : -1;  // halo layer written here
+      if (axis == 0) { c = in + 8 * i + 64 * j; h = hidx(out, i, j); }
+      else if (axis == 1) { c = i + 8 * in + 64 * j; h = hidx(i, out, j); }
+      else { c = i + 8 * j + 64 * in; h = hidx(i, j, out); }
+    }
+    if (src >= 0) {
+      const TileHdr* S = tiles + src;
+      const uint32_t m = S->emask[c >> 5], bit = 1u << (c & 31);
+      if (m & bit) E[h] = vb[(size_t)src * kBrickCells + S->epre[c >> 5] + __popc(m & (bit - 1u))];
+    }
+  }
+  __syncthreads();
   const double s = scale ? __ldg(scale + (size_t)T->pad[2] * lds) : 1.0;
-  for (int a = a0 + threadIdx.x; a < a1; a += blockDim.x) {
-    const int c = __ldg(acell + a);
-    const int lx = c & 7, ly = (c >> 3) & 7, lz = c >> 6;
-    double sum;
-    sum = (lx < 7) ? vt[c + 1] : vb[(size_t)n0 * kBrickCells + c - 7];
-    sum += (lx > 0) ? vt[c - 1] : vb[(size_t)n1 * kBrickCells + c + 7];
-    sum += (ly < 7) ? vt[c + 8] : vb[(size_t)n2 * kBrickCells + c - 56];
-    sum += (ly > 0) ? vt[c - 8] : vb[(size_t)n3 * kBrickCells + c + 56];
-    sum += (lz < 7) ? vt[c + 64] : vb[(size_t)n4 * kBrickCells + c - 448];
-    sum += (lz > 0) ? vt[c - 64] : vb[(size_t)n5 * kBrickCells + c + 448];
-    y[a] = s * (diag * __ldg(u + a) - ih2 * sum);
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const int a = a0 + tid + k * kLapThreads;
+    if (a < a1) {
+      const int c = ac[k];
+      const int h = hidx(c & 7, (c >> 3) & 7, c >> 6);
+      const double sum = E[h + 1] + E[h - 1] + E[h + 10] + E[h - 10] + E[h + 100] + E[h - 100];
+      y[a] = s * (diag * au[k] - ih2 * sum);
+    }
   }
 }
 
-bool g_attr_set = false;
-int g_sms = 0;
 
 }  // namespace
 
@@ -213,36 +258,31 @@ int apply_device(const cpm_band* b, double c, const double* u, double* y, const 
 
 int apply_device_split(const cpm_band* b, double c, const double* u, const double* uh, double* y,
                        const double* scale, int lds, cudaStream_t s) {
-  const size_t smemMax = 2 * (size_t)kMaxBoxCells * sizeof(double);
-  if (!g_attr_set) {
-    CPM_CUDA(cudaFuncSetAttribute(k_extend<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)smemMax));
-    CPM_CUDA(cudaFuncSetAttribute(k_extend<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)smemMax));
-    int dev = 0;
-    CPM_CUDA(cudaGetDevice(&dev));
-    CPM_CUDA(cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev));
-    g_attr_set = true;
-  }
-  const size_t smem = 2 * (size_t)b->maxBox * sizeof(double);
-  // CTAs per SM limited by shared memory (227 KB usable) and the launch bound
-  const int per_sm = std::max(1, std::min<int>(kExtMinBlocks, (int)((227 * 1024) / (smem + 1024))));
-  const int grid = std::max(1, std::min(b->nT, g_sms * per_sm));
   const double ih2 = 1.0 / (b->h * b->h);
   const double diag = c + 6.0 * ih2;
   {
+    const int descCap = 512;
+    const size_t smem = (size_t)b->maxBox * 8 + (size_t)descCap * 8;
     ProfScope ps(K_EXTEND, s);
-    if (b->zeroFill)
-      k_extend<true><<<grid, kExtThreads, smem, s>>>(b->tiles, b->nT, b->maxBox, b->runs, u, uh,
-                                                     b->srcSplit, b->tx, b->ty, b->tz, b->eoff, b->vb);
-    else
-      k_extend<false><<<grid, kExtThreads, smem, s>>>(b->tiles, b->nT, b->maxBox, b->runs, u, uh,
-                                                      b->srcSplit, b->tx, b->ty, b->tz, b->eoff, b->vb);
+#define CPM_EXTNT(Z)                                                                         \
+  do {                                                                                       \
+    static bool attr = false;                                                                \
+    if (!attr) {                                                                             \
+      CPM_CUDA(cudaFuncSetAttribute(k_extend_nt<Z>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                    227 * 1024));                                            \
+      attr = true;                                                                           \
+    }                                                                                        \
+    k_extend_nt<Z><<<b->nT, kNtThreads, smem, s>>>(b->tiles, b->maxBox, descCap, b->runs, u, uh, \
+                                                   b->srcSplit, b->tx, b->ty, b->tz, b->eoff,   \
+                                                   b->vb);                                      \
+  } while (0)
+    if (b->zeroFill) CPM_EXTNT(true); else CPM_EXTNT(false);
+#undef CPM_EXTNT
     count_launch();
   }
   {
     ProfScope ps(K_LAPLACE, s);
-    k_laplace<<<b->nT, 256, 0, s>>>(b->tiles, u, b->acell, b->vb, y, diag, ih2, scale, lds);
+    k_laplace<<<b->nT, kLapThreads, 0, s>>>(b->tiles, u, b->acell, b->vb, y, diag, ih2, scale, lds);
     count_launch();
   }
   CPM_CUDA(cudaGetLastError());

@@ -128,12 +128,17 @@ __global__ void k_compact_tiles(int nb, const int* ne, const int* tslot, const i
   T.a1 = astart[b] + na[b];
   morton_brick(keys[b], &T.bx, &T.by, &T.bz);
   for (int q = 0; q < 6; ++q) T.nbr[q] = -1;
-  tiles[t] = T;
   tgstart[t] = gstart[b];
   for (int q = 0; q < 16; ++q) {
     tam[(size_t)t * 16 + q] = amask[(size_t)b * 16 + q];
     tgm[(size_t)t * 16 + q] = gmask[(size_t)b * 16 + q];
+    T.emask[q] = amask[(size_t)b * 16 + q] | gmask[(size_t)b * 16 + q];
   }
+  for (int q = 0, r = 0; q < 16; ++q) {
+    T.epre[q] = (uint16_t)r;
+    r += __popc(T.emask[q]);
+  }
+  tiles[t] = T;
 }
 
 // ------------------------------------------------------------------ B5
@@ -290,7 +295,7 @@ __global__ void k_eoff(int nT, const TileHdr* tiles, const int32_t* ebase, const
   for (int e = T.e0 + threadIdx.x; e < T.e1; e += blockDim.x) {
     int b0 = ebase[3 * (size_t)e], b1 = ebase[3 * (size_t)e + 1], b2 = ebase[3 * (size_t)e + 2];
     uint32_t off = (uint32_t)((b0 - T.ox) + T.pad[0] * (b1 - T.oy) + T.pad[1] * (b2 - T.oz));
-    eoff[e] = off | ((uint32_t)ecell[e] << 16);
+    eoff[e] = off | ((uint32_t)emask_rank(T.emask, ecell[e]) << 16);  // vb slot (compact)
     bool ok = true;
     for (int cz = 0; cz < 4 && ok; ++cz)
       for (int cy = 0; cy < 4 && ok; ++cy)
@@ -351,30 +356,110 @@ __global__ void __launch_bounds__(512) k_sort_tile(const TileHdr* tiles, double*
   }
 }
 
+// ------------------------------------------------------------------ B6c
+// Half-warp order: k_extend_nt gives the tile's nodes 16 at a time to the lanes
+// of a half-warp, whose 8-byte shared-memory gathers are conflict-free when the
+// distinct stencil bases among the 16 fall in distinct banks (box offset mod 16;
+// lanes with the same base read the same address: a broadcast).  Greedy, from
+// the base-sorted order: a half-warp takes the next compatible nodes, and only
+// when none is left any remaining ones.  One CTA per tile, thread 0 plans.
+__global__ void __launch_bounds__(512) k_halfwarp_order(const TileHdr* tiles, double* tx, double* ty,
+                                                        double* tz, uint32_t* eoff) {
+  __shared__ double sv[3][512];
+  __shared__ uint32_t so[512];
+  __shared__ uint16_t perm[512];
+  __shared__ uint8_t used[512];
+  const TileHdr T = tiles[blockIdx.x];
+  const int n = T.e1 - T.e0, t = threadIdx.x;
+  if (t < n) {
+    sv[0][t] = tx[T.e0 + t];
+    sv[1][t] = ty[T.e0 + t];
+    sv[2][t] = tz[T.e0 + t];
+    so[t] = eoff[T.e0 + t];
+    used[t] = 0;
+  }
+  __syncthreads();
+  if (t == 0) {
+    int out = 0, first = 0;
+    while (out < n) {
+      uint32_t res = 0;
+      uint16_t offs[16];
+      int taken = 0;
+      for (int i = first; i < n && taken < 16; ++i) {
+        if (used[i]) continue;
+        const uint32_t o = so[i] & 0xffffu;
+        bool ok = !((res >> (o & 15)) & 1u);
+        for (int q = 0; q < taken && !ok; ++q) ok = offs[q] == o;
+        if (!ok) continue;
+        res |= 1u << (o & 15);
+        offs[taken++] = (uint16_t)o;
+        used[i] = 1;
+        perm[out++] = (uint16_t)i;
+      }
+      for (int i = first; i < n && taken < 16; ++i) {  // nothing compatible left
+        if (used[i]) continue;
+        used[i] = 1;
+        perm[out++] = (uint16_t)i;
+        ++taken;
+      }
+      while (first < n && used[first]) ++first;
+    }
+  }
+  __syncthreads();
+  if (t < n) {
+    const int o = perm[t];
+    tx[T.e0 + t] = sv[0][o];
+    ty[T.e0 + t] = sv[1][o];
+    tz[T.e0 + t] = sv[2][o];
+    eoff[T.e0 + t] = so[o];
+  }
+}
+
 // ------------------------------------------------------------------ B7
 // Thread per (tile, box row).  Walk the row's x range brick by brick; maximal
 // segments of consecutive Sigma_A cells inside one brick row are consecutive in
 // band order and become one run (source = band-order index of the first cell).
 __global__ void k_rows_per_tile(int nT, const TileHdr* tiles, int64_t* nrows) {
   int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t < nT) nrows[t] = (int64_t)tiles[t].sy * tiles[t].sz;
+  if (t < nT) nrows[t] = (int64_t)tiles[t].sy * tiles[t].sz + 1;  // + the alignment row
   if (t == 0) nrows[nT] = 0;
 }
 
+// Only the cells some stencil of the tile reads are staged: per box row the x
+// range is the union of the stencil rows' [b0, b0 + 3] that fall on it.
 template <bool WRITE>
-__global__ void k_runs(const TileHdr* tiles, const uint32_t* tam, const int* bmap, const int* blo,
-                       const int* bdim, const int64_t* rowbase, int64_t* rowcnt,
-                       const int64_t* runstart, uint64_t* runs) {
+__global__ void k_runs(const TileHdr* tiles, const int32_t* ebase, const uint32_t* tam,
+                       const int* bmap, const int* blo, const int* bdim, const int64_t* rowbase,
+                       int64_t* rowcnt, const int64_t* runstart, uint64_t* runs) {
+  __shared__ int xlo[kMaxBoxEdge * kMaxBoxEdge], xhi[kMaxBoxEdge * kMaxBoxEdge];
+  __shared__ int tot;
   int t = blockIdx.x;
   const TileHdr T = tiles[t];
   int nrows = T.sy * T.sz;
+  for (int r = threadIdx.x; r < nrows; r += blockDim.x) {
+    xlo[r] = INT_MAX;
+    xhi[r] = INT_MIN;
+  }
+  if (threadIdx.x == 0) tot = 0;
+  __syncthreads();
+  for (int e = T.e0 + threadIdx.x; e < T.e1; e += blockDim.x) {
+    const int b0 = ebase[3 * (size_t)e], b1 = ebase[3 * (size_t)e + 1] - T.oy,
+              b2 = ebase[3 * (size_t)e + 2] - T.oz;
+    for (int dz = 0; dz < 4; ++dz)
+      for (int dy = 0; dy < 4; ++dy) {
+        const int r = (b1 + dy) + T.sy * (b2 + dz);
+        atomicMin(&xlo[r], b0);
+        atomicMax(&xhi[r], b0 + 4);
+      }
+  }
+  __syncthreads();
   for (int r = threadIdx.x; r < nrows; r += blockDim.x) {
     int y = T.oy + r % T.sy, z = T.oz + r / T.sy;
     int by = brick_of(y), bz = brick_of(z), ly = local_of(y), lz = local_of(z);
     int64_t gi = rowbase[t] + r;
     int64_t out = WRITE ? runstart[gi] : 0;
     int64_t n = 0;
-    int x = T.ox, xe = T.ox + T.sx;
+    int x = xlo[r], xe = xhi[r];  // empty row: x = INT_MAX > xe
     while (x < xe) {
       int bx = brick_of(x);
       int xend = min(xe, bx * 8 + 8);
@@ -399,7 +484,22 @@ __global__ void k_runs(const TileHdr* tiles, const uint32_t* tam, const int* bma
       }
       x = xend;
     }
-    if (!WRITE) rowcnt[gi] = n;
+    if (!WRITE) {
+      rowcnt[gi] = n;
+      atomicAdd(&tot, (int)n);
+    }
+  }
+  // alignment row: one empty run when the tile has an odd number of runs, so
+  // every tile's run range starts 16-byte aligned (bulk copies)
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int64_t gi = rowbase[t] + nrows;
+    if (WRITE) {
+      if (rowbase[t + 1] - rowbase[t] == nrows + 1 && runstart[gi + 1] > runstart[gi])
+        runs[runstart[gi]] = 0ull;
+    } else {
+      rowcnt[gi] = tot & 1;
+    }
   }
 }
 
@@ -409,6 +509,13 @@ __global__ void k_set_run_ranges(int nT, TileHdr* tiles, const int64_t* rowbase,
   if (t >= nT) return;
   tiles[t].r0 = (int32_t)runstart[rowbase[t]];
   tiles[t].r1 = (int32_t)runstart[rowbase[t + 1]];
+}
+
+// eval ranges start at multiples of 4 nodes (16-byte aligned for bulk copies)
+__global__ void k_round4(int nb, const int* ne, int* ne4) {
+  int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b < nb) ne4[b] = (ne[b] + 3) & ~3;
+  if (b == 0) ne4[nb] = 0;
 }
 
 __global__ void k_flags(int nb, const int* ne, int* flag) {
@@ -481,8 +588,9 @@ void free_band(cpm_band* b) {
   if (!b) return;
   if (b->ws) free_workspace(b->ws);
   if (b->owns) {
-    void* ptrs[] = {b->tiles, b->tx, b->ty,      b->tz,      b->eoff,  b->acell, b->aijk,
-                    b->gijk,  b->runs, b->vb, b->dstage0, b->dstage1, b->amask, b->bmap};
+    void* ptrs[] = {b->tiles, b->tx,      b->ty,      b->tz,    b->eoff, b->acell,
+                    b->aijk,  b->gijk,    b->runs,    b->vb,    b->dstage0, b->dstage1,
+                    b->amask, b->bmap};
     for (void* p : ptrs)
       if (p) cudaFree(p);
   } else {  // sub-band: owns only its own tiles/runs/acell/vb
@@ -580,7 +688,13 @@ int build_band(const cpm_surface* surf, double h, int p, double L, cudaStream_t 
   CPM_TRY(dalloc<int>(tslot, nb + 1, "tslot"));
   CPM_TRY(exclusive_sum(na.as<int>(), astart.as<int>(), nb + 1, s));
   CPM_TRY(exclusive_sum(ng.as<int>(), gstart.as<int>(), nb + 1, s));
-  CPM_TRY(exclusive_sum(ne.as<int>(), estart.as<int>(), nb + 1, s));
+  {
+    DevBuf ne4;
+    CPM_TRY(dalloc<int>(ne4, nb + 1, "ne4"));
+    k_round4<<<grid_for(nb + 1, 256), 256, 0, s>>>(nb, ne.as<int>(), ne4.as<int>());
+    count_launch();
+    CPM_TRY(exclusive_sum(ne4.as<int>(), estart.as<int>(), nb + 1, s));
+  }
   k_flags<<<grid_for(nb, 256), 256, 0, s>>>(nb, ne.as<int>(), flag.as<int>());
   count_launch();
   CPM_TRY(exclusive_sum(flag.as<int>(), tslot.as<int>(), nb + 1, s));
@@ -625,10 +739,10 @@ int build_band(const cpm_surface* surf, double h, int p, double L, cudaStream_t 
   CPM_TRY(dalloc_owned(&B->aijk, 3 * (size_t)totA, &B->bytes, "aijk"));
   CPM_TRY(dalloc_owned(&B->gijk, 3 * (size_t)std::max(totG, 1), &B->bytes, "gijk"));
   CPM_TRY(dalloc_owned(&B->acell, totA, &B->bytes, "acell"));
-  CPM_TRY(dalloc_owned(&B->tx, totE, &B->bytes, "tx"));
-  CPM_TRY(dalloc_owned(&B->ty, totE, &B->bytes, "ty"));
-  CPM_TRY(dalloc_owned(&B->tz, totE, &B->bytes, "tz"));
-  CPM_TRY(dalloc_owned(&B->eoff, totE, &B->bytes, "eoff"));
+  CPM_TRY(dalloc_owned(&B->tx, (size_t)totE + 8, &B->bytes, "tx"));
+  CPM_TRY(dalloc_owned(&B->ty, (size_t)totE + 8, &B->bytes, "ty"));
+  CPM_TRY(dalloc_owned(&B->tz, (size_t)totE + 8, &B->bytes, "tz"));
+  CPM_TRY(dalloc_owned(&B->eoff, (size_t)totE + 8, &B->bytes, "eoff"));
   CPM_TRY(dalloc<int32_t>(ebase, 3 * (size_t)totE, "ebase"));
   CPM_TRY(dalloc<uint16_t>(ecell, totE, "ecell"));
   CPM_TRY(dalloc<int>(err, 2, "err"));
@@ -679,6 +793,11 @@ int build_band(const cpm_surface* surf, double h, int p, double L, cudaStream_t 
   count_launch();
   CPM_CUDA(cudaGetLastError());
 
+  // B6c half-warp order
+  k_halfwarp_order<<<totT, 512, 0, s>>>(B->tiles, B->tx, B->ty, B->tz, B->eoff);
+  count_launch();
+  CPM_CUDA(cudaGetLastError());
+
   // B7 fill runs
   DevBuf nrows, rowbase, rowcnt, runstart;
   CPM_TRY(dalloc<int64_t>(nrows, totT + 1, "nrows"));
@@ -691,7 +810,7 @@ int build_band(const cpm_surface* surf, double h, int p, double L, cudaStream_t 
   CPM_TRY(dalloc<int64_t>(rowcnt, totRows + 1, "rowcnt"));
   CPM_TRY(dalloc<int64_t>(runstart, totRows + 1, "runstart"));
   CPM_CUDA(cudaMemsetAsync(rowcnt.p, 0, (totRows + 1) * sizeof(int64_t), s));
-  k_runs<false><<<totT, 128, 0, s>>>(B->tiles, tam.as<uint32_t>(), bmap.as<int>(), dblo.as<int>(),
+  k_runs<false><<<totT, 128, 0, s>>>(B->tiles, ebase.as<int32_t>(), tam.as<uint32_t>(), bmap.as<int>(), dblo.as<int>(),
                                      dbdim.as<int>(), rowbase.as<int64_t>(), rowcnt.as<int64_t>(),
                                      nullptr, nullptr);
   count_launch();
@@ -699,8 +818,8 @@ int build_band(const cpm_surface* surf, double h, int p, double L, cudaStream_t 
   int64_t totRuns = 0;
   CPM_TRY(read_back(runstart.as<int64_t>() + totRows, &totRuns, s));
   if (totRuns >= (int64_t)INT32_MAX) return fail(CPM_ERR_LIMIT, "cpm_build_band: too many runs");
-  CPM_TRY(dalloc_owned(&B->runs, totRuns, &B->bytes, "runs"));
-  k_runs<true><<<totT, 128, 0, s>>>(B->tiles, tam.as<uint32_t>(), bmap.as<int>(), dblo.as<int>(),
+  CPM_TRY(dalloc_owned(&B->runs, (size_t)totRuns + 2, &B->bytes, "runs"));
+  k_runs<true><<<totT, 128, 0, s>>>(B->tiles, ebase.as<int32_t>(), tam.as<uint32_t>(), bmap.as<int>(), dblo.as<int>(),
                                     dbdim.as<int>(), rowbase.as<int64_t>(), rowcnt.as<int64_t>(),
                                     runstart.as<int64_t>(), B->runs);
   count_launch();

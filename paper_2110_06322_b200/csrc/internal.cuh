@@ -47,7 +47,10 @@ struct ProfScope {
 void count_launch();
 
 // ------------------------------------------------------------------ band data
-// One tile = one occupied 8^3 brick.  64-bit aligned, 96 bytes.
+// One tile = one occupied 8^3 brick.  64-bit aligned, 192 bytes.
+// E u of the tile's eval nodes lives in vb[slot * 512 + rank], rank = position of
+// the node's brick cell among the set bits of emask (cell order), so a tile's
+// values are contiguous (compact) and any cell is located by a popcount.
 struct TileHdr {
   int32_t e0, e1;      // eval nodes (Sigma_A u Sigma_G in the brick) [e0, e1)
   int32_t a0, a1;      // output (active / owned) nodes [a0, a1)
@@ -56,9 +59,24 @@ struct TileHdr {
   int32_t sx, sy, sz;  // stencil box extent (cells)
   int32_t nbr[6];      // face neighbour tile slots (+x,-x,+y,-y,+z,-z), -1 = none
   int32_t bx, by, bz;  // brick coordinates (lattice origin = 8*b)
-  int32_t pad[3];
+  int32_t pad[3];      // row stride, plane stride of the box; segment id (RAS)
+  uint32_t emask[16];  // eval-node cells of the brick (Sigma_A u Sigma_G), bit = cell
+  uint16_t epre[16];   // epre[w] = set bits of emask[0..w)
 };
-static_assert(sizeof(TileHdr) == 96, "TileHdr layout");
+static_assert(sizeof(TileHdr) == 192, "TileHdr layout");
+
+__host__ __device__ inline int popc32(uint32_t v) {
+#ifdef __CUDA_ARCH__
+  return __popc(v);
+#else
+  return __builtin_popcount(v);
+#endif
+}
+__host__ __device__ inline int emask_rank(const uint32_t* m16, int cell) {
+  int w = cell >> 5, r = 0;
+  for (int q = 0; q < w; ++q) r += popc32(m16[q]);
+  return r + popc32(m16[w] & ((1u << (cell & 31)) - 1u));
+}
 
 // A fill run copies len consecutive source doubles u[src..src+len) to
 // box[dst..dst+len).  Packed: src (bits 0-31), dst (32-47), len (48-55).
@@ -93,7 +111,7 @@ struct cpm_band {
   double* tx = nullptr;            // nE fractional offsets (SoA)
   double* ty = nullptr;
   double* tz = nullptr;
-  uint32_t* eoff = nullptr;        // nE: box offset (low 16) | brick cell (high 16)
+  uint32_t* eoff = nullptr;        // nE: box offset (low 16) | vb rank in the tile (high 16)
   uint16_t* acell = nullptr;       // nA: brick cell of each output node
   int32_t* aijk = nullptr;         // 3*nA lattice coords (band order)
   int32_t* gijk = nullptr;         // 3*nG lattice coords

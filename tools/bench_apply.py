@@ -1,4 +1,8 @@
-"""Quick apply / GMRES-kernel timing on config 1 (for iterating on kernels)."""
+"""Quick apply timing on config 1 (for iterating on kernels).
+
+CPM_KS="1 2 3 4" times the apply for each node-group size K (band rebuilt per K)
+and checks that all K give the same result (up to rounding).
+"""
 import os
 import sys
 
@@ -10,33 +14,42 @@ import paper_2110_06322_b200 as cpm
 import seeded_inputs
 
 h = float(os.environ.get("CPM_H", 1.0 / 200))
-band = cpm.cpm_build_band("sphere", h)
-coords = cpm.cpm_band_active_coords(band).astype(np.int64)
-u = torch.from_numpy(seeded_inputs.uniform_pm1(0, coords)).cuda()
-y = torch.empty_like(u)
-for _ in range(5):
-    cpm.cpm_apply(band, 10.0, u, y)
-torch.cuda.synchronize()
-cpm.cpm_profile_reset()
-cpm.cpm_profile_enable(True)
-N = 50
-a = torch.cuda.Event(enable_timing=True)
-b = torch.cuda.Event(enable_timing=True)
-a.record()
-for _ in range(N):
-    cpm.cpm_apply(band, 10.0, u, y)
-b.record()
-torch.cuda.synchronize()
-cpm.cpm_profile_enable(False)
-ms = a.elapsed_time(b) / N
-e, _ = cpm.cpm_profile_read("extend")
-l, _ = cpm.cpm_profile_read("laplace")
-nA, nG = band.info.n_active, band.info.n_ghost
-alg = 16 * nA + 28 * (nA + nG)
-print(f"nA={nA} tiles={band.info.n_tiles} maxbox={band.info.max_box} apply {ms*1e3:.1f} us "
-      f"(extend {e/N*1e3:.1f} us, laplace {l/N*1e3:.1f} us) -> {alg/ms/1e6:.0f} GB/s alg, "
-      f"{nA/ms/1e6:.2f} Gnodes/s")
+ks = [int(k) for k in os.environ.get("CPM_KS", "4").split()]
+ref = None
+for K in ks:
+    os.environ["CPM_GROUP_K"] = str(K)
+    band = cpm.cpm_build_band("sphere", h)
+    coords = cpm.cpm_band_active_coords(band).astype(np.int64)
+    u = torch.from_numpy(seeded_inputs.uniform_pm1(0, coords)).cuda()
+    y = torch.empty_like(u)
+    for _ in range(5):
+        cpm.cpm_apply(band, 10.0, u, y)
+    torch.cuda.synchronize()
+    if ref is None:
+        ref = y.clone()
+    err = float((y - ref).abs().max() / ref.abs().max())
+    cpm.cpm_profile_reset()
+    cpm.cpm_profile_enable(True)
+    N = 50
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(N):
+        cpm.cpm_apply(band, 10.0, u, y)
+    b.record()
+    torch.cuda.synchronize()
+    cpm.cpm_profile_enable(False)
+    ms = a.elapsed_time(b) / N
+    e, _ = cpm.cpm_profile_read("extend")
+    l, _ = cpm.cpm_profile_read("laplace")
+    nA, nG = band.info.n_active, band.info.n_ghost
+    alg = 16 * nA + 28 * (nA + nG)
+    print(f"K={K} nA={nA} tiles={band.info.n_tiles} runs={band.info.n_runs} maxbox={band.info.max_box} "
+          f"apply {ms*1e3:.1f} us (extend {e/N*1e3:.1f} us, laplace {l/N*1e3:.1f} us) -> "
+          f"{alg/ms/1e6:.0f} GB/s alg, {nA/ms/1e6:.2f} Gnodes/s, diff vs first K {err:.1e}", flush=True)
+    del band
 if os.environ.get("CPM_SOLVE"):
+    band = cpm.cpm_build_band("sphere", h)
     f = torch.empty_like(u)
     cpm.cpm_eval_sph(band, 6, 3, 52.0, f)
     x = torch.zeros_like(u)
