@@ -4,22 +4,21 @@
 //     = (c + 6/h^2) u - (1/h^2) sum_{6 nbrs j} (E u)_j    (the centre (E u)_i terms cancel)
 //
 // Two kernels per apply:
-//   k_extend  (persistent, one tile = occupied 8^3 brick at a time per CTA):
-//             stage the cells of u the tile's stencils read into a shared-memory
-//             box (fill runs of consecutive band-order sources, 8 lanes per run,
-//             cp.async), prefetching the next tile's box and node offsets while the
-//             current tile is contracted; for every eval node (Sigma_A u Sigma_G in
+//   k_extend_nt (one CTA of 128 threads per tile = occupied 8^3 brick, up to 4
+//             eval nodes per thread): stage the cells of u the tile's stencils read
+//             into a shared-memory box (fill runs of consecutive band-order sources,
+//             8 lanes per run, cp.async); for every eval node (Sigma_A u Sigma_G in
 //             the brick) recompute the tricubic Lagrange weights from its fractional
-//             offsets and contract x, then y, then z.  Nodes of a tile
-//             are sorted by stencil base, so the lanes of a warp read overlapping
-//             stencils (shared-memory broadcast).  E u goes to the tile's compact
+//             offsets and contract x, then y, then z.  A tile's nodes
+//             are ordered (build time) so the 16 lanes of a half-warp read distinct
+//             banks or the same address (broadcast).  E u goes to the tile's compact
 //             slot range of vb (cell order, TileHdr::emask ranks).
-//   k_laplace (one CTA per tile): gather the tile's E u and the face layers of its
-//             6 neighbour tiles into a dense 10^3 halo brick in shared memory, then
-//             the 7-point combination for every output node.
-// HBM-bound by design (no tensor cores: this is a gather, not a dense
-// contraction).  Node offsets are streamed with evict-first loads so that u and
-// vb stay resident in the 126 MB L2 between the two kernels.
+//   k_laplace (one CTA of 128 threads per tile): gather the tile's E u and the face
+//             layers of its 6 neighbour tiles into a dense 10^3 halo brick in shared
+//             memory, then the 7-point combination for every output node.
+// No tensor cores: this is a gather, not a dense contraction.  The extend is
+// bound by shared-memory wavefronts (64 8-byte gathers per node) and FP64 issue,
+// the laplace by load latency; DESIGN.md §Kernels has the measured rooflines.
 #include <algorithm>
 
 #include "internal.cuh"
@@ -181,11 +180,11 @@ __global__ void __launch_bounds__(kNtThreads, 8)
 // Dense halo brick: cell (x, y, z), x, y, z in -1..8, at (x+1) + 10 (y+1) + 100 (z+1).
 __device__ __forceinline__ int hidx(int x, int y, int z) { return (x + 1) + 10 * (y + 1) + 100 * (z + 1); }
 
-constexpr int kLapThreads = 256;
 
 // One CTA per tile.  All global loads (own E u, the neighbours' face layers, the
 // output nodes' u and cells) are issued before the single barrier, so a CTA has
 // one dependent chain: header -> neighbour header -> vb.
+template <int kLapThreads>
 __global__ void __launch_bounds__(kLapThreads) k_laplace(const TileHdr* __restrict__ tiles,
                                                          const double* __restrict__ u,
                                                          const uint16_t* __restrict__ acell,
@@ -198,20 +197,21 @@ __global__ void __launch_bounds__(kLapThreads) k_laplace(const TileHdr* __restri
   const TileHdr* T = tiles + t;
   const int a0 = T->a0, a1 = T->a1;
   if (a0 == a1) return;
-  // output nodes: up to 2 per thread
-  int ac[2];
-  double au[2];
+  constexpr int kOut = kBrickCells / kLapThreads, kGat = (kBrickCells + 384 + kLapThreads - 1) / kLapThreads;
+  // output nodes: up to kOut per thread
+  int ac[kOut];
+  double au[kOut];
 #pragma unroll
-  for (int k = 0; k < 2; ++k) {
+  for (int k = 0; k < kOut; ++k) {
     const int a = a0 + tid + k * kLapThreads;
     if (a < a1) {
       ac[k] = __ldg(acell + a);
       au[k] = __ldg(u + a);
     }
   }
-  // 512 own cells + 6 x 64 face cells of the neighbours: 3.5 per thread
+  // 512 own cells + 6 x 64 face cells of the neighbours
 #pragma unroll
-  for (int k = 0; k < 4; ++k) {
+  for (int k = 0; k < kGat; ++k) {
     const int q = tid + k * kLapThreads;
     int src = -1, c = 0, h = 0;
     if (q < kBrickCells) {
@@ -237,7 +237,7 @@ __global__ void __launch_bounds__(kLapThreads) k_laplace(const TileHdr* __restri
   __syncthreads();
   const double s = scale ? __ldg(scale + (size_t)T->pad[2] * lds) : 1.0;
 #pragma unroll
-  for (int k = 0; k < 2; ++k) {
+  for (int k = 0; k < kOut; ++k) {
     const int a = a0 + tid + k * kLapThreads;
     if (a < a1) {
       const int c = ac[k];
@@ -282,7 +282,8 @@ int apply_device_split(const cpm_band* b, double c, const double* u, const doubl
   }
   {
     ProfScope ps(K_LAPLACE, s);
-    k_laplace<<<b->nT, kLapThreads, 0, s>>>(b->tiles, u, b->acell, b->vb, y, diag, ih2, scale, lds);
+    // 128 threads per tile: 16 resident tiles per SM keep enough loads in flight
+    k_laplace<128><<<b->nT, 128, 0, s>>>(b->tiles, u, b->acell, b->vb, y, diag, ih2, scale, lds);
     count_launch();
   }
   CPM_CUDA(cudaGetLastError());

@@ -32,49 +32,62 @@ namespace cpm {
 
 // ---------------------------------------------------------------- launch helpers
 namespace {
-inline int kmax_bucket(int k) { return k <= 8 ? 8 : k <= 16 ? 16 : k <= 32 ? 32 : 64; }
 constexpr int VB = vec::VB;
+}  // namespace
+
+namespace {
+template <int MODE>
+int launch_proj(const vec::Seg& S, int k, const double* V, int64_t ldv, double* w, const double* sc,
+                int lds, const double* coef, int ldc, double* vout, double* partial, int pld,
+                double* out, int ldo, unsigned* counters, cudaStream_t st) {
+  const int grid = S.nseg * S.gps;
+  if (k < 1 || k > kMaxRestart) return fail(CPM_ERR_ARG, "Krylov projection: k out of range");
+  if (k <= 64) {
+    const size_t sm = vec::proj_smem<256>(k);
+    static bool attr = false;
+    if (!attr) {
+      CPM_CUDA(cudaFuncSetAttribute(vec::k_proj<MODE, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)vec::proj_smem<256>(64)));
+      attr = true;
+    }
+    vec::k_proj<MODE, 256><<<grid, 256, sm, st>>>(S, k, V, ldv, w, sc, lds, coef, ldc, vout, partial,
+                                                   pld, out, ldo, counters);
+  } else {
+    const size_t sm = vec::proj_smem<128>(k);
+    static bool attr = false;
+    if (!attr) {
+      CPM_CUDA(cudaFuncSetAttribute(vec::k_proj<MODE, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)vec::proj_smem<128>(kMaxRestart + 2)));
+      attr = true;
+    }
+    vec::k_proj<MODE, 128><<<grid, 128, sm, st>>>(S, k, V, ldv, w, sc, lds, coef, ldc, vout, partial,
+                                                   pld, out, ldo, counters);
+  }
+  count_launch();
+  CPM_CUDA(cudaGetLastError());
+  return CPM_OK;
+}
 }  // namespace
 
 int launch_mdot(const vec::Seg& S, int k, const double* V, int64_t ldv, const double* w,
                 const double* sc, int lds, double* partial, double* out, int ldo,
                 unsigned* counters, cudaStream_t st) {
-  vec::k_mdot8<<<S.nseg * S.gps, VB, 0, st>>>(S, k, V, ldv, w, sc, lds, partial, kMaxRestart + 8,
-                                              out, ldo, counters);
-  count_launch();
-  CPM_CUDA(cudaGetLastError());
-  return CPM_OK;
+  return launch_proj<0>(S, k, V, ldv, const_cast<double*>(w), sc, lds, nullptr, 0, nullptr, partial,
+                        kMaxRestart + 8, out, ldo, counters, st);
 }
 
 int launch_cgs_final(const vec::Seg& S, int k, const double* V, int64_t ldv, const double* w,
                      const double* sc, int lds, const double* coef, int ldo, double* vout,
                      double* partial, double* out, int ldn, unsigned* counters, cudaStream_t st) {
-  vec::k_cgs_final<<<S.nseg * S.gps, VB, 0, st>>>(S, k, V, ldv, w, sc, lds, coef, ldo, vout, partial,
-                                                  out, ldn, counters);
-  count_launch();
-  CPM_CUDA(cudaGetLastError());
-  return CPM_OK;
+  return launch_proj<2>(S, k, V, ldv, const_cast<double*>(w), sc, lds, coef, ldo, vout, partial, 1,
+                        out, ldn, counters, st);
 }
 
 int launch_cgs_update(const vec::Seg& S, int k, const double* V, int64_t ldv, double* w,
                       const double* sc, int lds, const double* coef, double* partial, double* out,
                       int ldo, unsigned* counters, cudaStream_t st) {
-  const int grid = S.nseg * S.gps;
-  switch (k <= 64 ? kmax_bucket(k) : 0) {
-    case 8: vec::k_cgs_update<8><<<grid, VB, 0, st>>>(S, k, V, ldv, w, sc, lds, coef, partial, out, ldo, counters); break;
-    case 16: vec::k_cgs_update<16><<<grid, VB, 0, st>>>(S, k, V, ldv, w, sc, lds, coef, partial, out, ldo, counters); break;
-    case 32: vec::k_cgs_update<32><<<grid, VB, 0, st>>>(S, k, V, ldv, w, sc, lds, coef, partial, out, ldo, counters); break;
-    case 64: vec::k_cgs_update<64><<<grid, VB, 0, st>>>(S, k, V, ldv, w, sc, lds, coef, partial, out, ldo, counters); break;
-    default: {
-      // k > 64: separate update (norm into a scratch slot) and dots
-      double* scratch = out + k;  // caller guarantees room for one extra value per segment
-      CPM_TRY(launch_cgs_final(S, k, V, ldv, w, sc, lds, coef, ldo, w, partial, scratch, ldo, counters, st));
-      return launch_mdot(S, k, V, ldv, w, sc, lds, partial, out, ldo, counters, st);
-    }
-  }
-  count_launch();
-  CPM_CUDA(cudaGetLastError());
-  return CPM_OK;
+  return launch_proj<1>(S, k, V, ldv, w, sc, lds, coef, ldo, nullptr, partial, kMaxRestart + 8, out,
+                        ldo, counters, st);
 }
 
 namespace {
@@ -166,7 +179,11 @@ int Workspace::ensure(int64_t n_, int m_, bool flex_) {
   int64_t off[2] = {0, n};
   CPM_CUDA(cudaMemcpy(segoff, off, sizeof(off), cudaMemcpyHostToDevice));
   const int64_t nsub = (n + vec::VB - 1) / vec::VB;
-  gps = (int)std::max<int64_t>(1, std::min<int64_t>(nsub, 148 * 8));
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  // 2 blocks per SM: each thread streams many elements; few partials to combine
+  gps = (int)std::max<int64_t>(1, std::min<int64_t>(nsub, 2 * (int64_t)sms));
   if (cudaMallocHost((void**)&hst, sizeof(HostState)) != cudaSuccess)
     return fail(CPM_ERR_NOMEM, "pinned host state allocation failed");
   return CPM_OK;

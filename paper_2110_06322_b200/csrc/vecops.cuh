@@ -29,10 +29,29 @@ struct Seg {
   int gps;             // blocks per segment
 };
 
+__device__ __forceinline__ void cp_commit_v() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_wait_all_v() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
+}
+
+// Sum partial[(base + b) * pld + i] over b < gps, lane-strided with 4 independent
+// accumulators (loads in flight), then across the warp.  Fixed order.
+__device__ __forceinline__ double partial_sum(const double* partial, size_t base, int pld, int gps,
+                                              int i, int lane) {
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  int b = lane;
+  for (; b + 96 < gps; b += 128) {
+    a0 += __ldcg(partial + (base + b) * pld + i);
+    a1 += __ldcg(partial + (base + b + 32) * pld + i);
+    a2 += __ldcg(partial + (base + b + 64) * pld + i);
+    a3 += __ldcg(partial + (base + b + 96) * pld + i);
+  }
+  for (; b < gps; b += 32) a0 += __ldcg(partial + (base + b) * pld + i);
+  return warp_sum((a0 + a1) + (a2 + a3));
 }
 
 // Reduce acc[0..k) over the block into partial[blockIdx.x * pld + i]; then the
@@ -67,9 +86,7 @@ __device__ __forceinline__ void block_then_segment_reduce(const double (&acc)[KM
   if (!last) return;
   __threadfence();
   for (int i = warp; i < k; i += VB / 32) {
-    double a = 0.0;
-    for (int b = lane; b < gps; b += 32) a += __ldcg(partial + (size_t)(s * gps + b) * pld + i);
-    a = warp_sum(a);
+    const double a = partial_sum(partial, (size_t)s * gps, pld, gps, i, lane);
     if (lane == 0) out[(size_t)s * ldo + i] = sc ? a * sc[(size_t)s * lds + i] : a;
   }
   if (threadIdx.x == 0) counters[s] = 0u;
@@ -122,12 +139,121 @@ static __global__ void __launch_bounds__(VB) k_mdot8(Seg S, int k, const double*
   if (!last) return;
   __threadfence();
   for (int i = warp; i < k; i += VB / 32) {
-    double a = 0.0;
-    for (int b = lane; b < S.gps; b += 32) a += __ldcg(partial + (size_t)(s * S.gps + b) * pld + i);
-    a = warp_sum(a);
+    const double a = partial_sum(partial, (size_t)s * S.gps, pld, S.gps, i, lane);
     if (lane == 0) out[(size_t)s * ldo + i] = sc ? a * sc[(size_t)s * lds + i] : a;
   }
   if (threadIdx.x == 0) counters[s] = 0u;
+}
+
+// ---------------------------------------------------------------- tile projections
+// One kernel per pass over the basis, MODE:
+//   0 (mdot)    out_i = sc_i <V_i, w>
+//   1 (update)  w <- w - sum_i cf_i V_i,  out_i = sc_i <V_i, w_new>      (cf_i = coef_i sc_i)
+//   2 (final)   vout <- w - sum_i cf_i V_i,  out_0 = ||vout||^2
+// A block of TB threads streams tiles of TB consecutive elements of its segment
+// (tiles lb, lb + gps, ... : fixed order).  Per tile every thread cp.async-copies
+// its element of V_0 .. V_{k-1} into shared memory (k independent 8-byte copies
+// in flight per thread: the pass runs at HBM bandwidth), forms its w value, and
+// for the dots the threads, grouped P per column, reduce the tile's column
+// products from shared memory.  V is read from HBM exactly once per pass.
+__device__ __forceinline__ void cpa8(void* smem, const void* gmem) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(a), "l"(gmem));
+}
+
+template <int MODE, int TB>
+static __global__ void __launch_bounds__(TB) k_proj(Seg S, int k, const double* __restrict__ V,
+                                                    int64_t ldv, double* w,
+                                                    const double* __restrict__ sc, int lds,
+                                                    const double* __restrict__ coef, int ldc,
+                                                    double* vout, double* partial, int pld,
+                                                    double* out, int ldo, unsigned* counters) {
+  constexpr int SV = TB + 4;  // padded column stride (bank spread of the column dots)
+  extern __shared__ double smp[];
+  double* sv = smp;            // k columns of SV
+  double* sw = sv + (size_t)k * SV;
+  double* cf = sw + TB;        // k
+  double* cs = cf + k;         // TB / 32 warp sums (MODE 2)
+  __shared__ bool last;
+  const int s = blockIdx.x / S.gps, lb = blockIdx.x % S.gps;
+  const int64_t o0 = S.off[s], n = S.off[s + 1] - o0;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (MODE != 0)
+    for (int i = tid; i < k; i += TB) cf[i] = coef[(size_t)s * ldc + i] * sc[(size_t)s * lds + i];
+  int kp = 8;
+  while (kp < k) kp <<= 1;
+  const int P = kp >= TB ? 1 : TB / kp;  // threads per column (<= 32 since kp >= 8... TB <= 256)
+  const int col = tid / P, sub = tid % P;
+  double acc = 0.0;
+  __syncthreads();
+  for (int64_t t0 = (int64_t)lb * TB; t0 < n; t0 += (int64_t)S.gps * TB) {
+    const int64_t e = t0 + tid;
+    const bool in = e < n;
+    if (in) {
+      const double* p = V + o0 + e;
+      for (int i = 0; i < k; ++i) cpa8(sv + (size_t)i * SV + tid, p + (size_t)i * ldv);
+    }
+    cp_commit_v();
+    double wv = in ? w[o0 + e] : 0.0;
+    cp_wait_all_v();
+    if (MODE != 0) {
+      double s0 = 0.0, s1 = 0.0;
+      if (in) {
+        int i = 0;
+        for (; i + 1 < k; i += 2) {
+          s0 += cf[i] * sv[(size_t)i * SV + tid];
+          s1 += cf[i + 1] * sv[(size_t)(i + 1) * SV + tid];
+        }
+        if (i < k) s0 += cf[i] * sv[(size_t)i * SV + tid];
+        wv -= s0 + s1;
+        if (MODE == 1) w[o0 + e] = wv;
+        else vout[o0 + e] = wv;
+      }
+      if (MODE == 2) acc += wv * wv;
+    }
+    if (MODE != 2) {
+      if (!in)
+        for (int i = 0; i < k; ++i) sv[(size_t)i * SV + tid] = 0.0;
+      sw[tid] = wv;
+      __syncthreads();
+      if (col < k) {
+        const double* c = sv + (size_t)col * SV;
+        for (int q = sub; q < TB; q += P) acc += c[q] * sw[q];
+      }
+      __syncthreads();
+    }
+  }
+  // block reduction -> partial[blockIdx.x * pld + i]
+  if (MODE == 2) {
+    double v = warp_sum(acc);
+    if (lane == 0) cs[warp] = v;
+    __syncthreads();
+    if (tid == 0) {
+      double t = 0.0;
+      for (int q = 0; q < TB / 32; ++q) t += cs[q];
+      partial[(size_t)blockIdx.x * pld] = t;
+    }
+  } else {
+    for (int o = P >> 1; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (sub == 0 && col < k) partial[(size_t)blockIdx.x * pld + col] = acc;
+  }
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) last = (atomicAdd(counters + s, 1u) == (unsigned)S.gps - 1u);
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  const int kout = MODE == 2 ? 1 : k;
+  for (int i = warp; i < kout; i += TB / 32) {
+    const double a = partial_sum(partial, (size_t)s * S.gps, pld, S.gps, i, lane);
+    if (lane == 0) out[(size_t)s * ldo + i] = (MODE != 2 && sc) ? a * sc[(size_t)s * lds + i] : a;
+  }
+  if (tid == 0) counters[s] = 0u;
+}
+
+template <int TB>
+inline size_t proj_smem(int k) {
+  return ((size_t)k * (TB + 4) + TB + (size_t)k + TB / 32) * sizeof(double);
 }
 
 // w <- w - sum_i coef_i sc_i V_i ;  out_i = sc_i <V_i, w_new>   (per segment)
