@@ -22,6 +22,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "internal.cuh"
@@ -91,6 +92,70 @@ int launch_cgs_update(const vec::Seg& S, int k, const double* V, int64_t ldv, do
 }
 
 namespace {
+constexpr int kLdc = kMaxRestart + 2;  // stride of GState::coef / red halves
+// unpreconditioned GMRES uses delayed CGS2 (2 passes per step); CPM_CGS2=1 forces
+// the 3-pass CGS2 of the flexible path (A/B measurements)
+const bool g_force_cgs2 = [] {
+  const char* v = getenv("CPM_CGS2");
+  return v && *v && *v != '0';
+}();
+
+int launch_dcgs_dots(const vec::Seg& S, int k, const double* V, int64_t ldv, const double* z,
+                     double* partial, double* out, unsigned* counters, cudaStream_t st) {
+  const int grid = S.nseg * S.gps;
+  const size_t sm = ((size_t)k * (256 + 4) + 256) * sizeof(double);
+  if (k <= 64) {
+    static bool attr = false;
+    if (!attr) {
+      CPM_CUDA(cudaFuncSetAttribute(vec::k_dcgs_dots<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)(((size_t)64 * 260 + 256) * sizeof(double))));
+      attr = true;
+    }
+    vec::k_dcgs_dots<256><<<grid, 256, sm, st>>>(S, k, V, ldv, z, partial, 2 * kLdc + 8, out, 0, counters);
+  } else {
+    static bool attr = false;
+    const size_t sm2 = ((size_t)k * (128 + 4) + 128) * sizeof(double);
+    if (!attr) {
+      CPM_CUDA(cudaFuncSetAttribute(vec::k_dcgs_dots<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)(((size_t)(kMaxRestart + 1) * 132 + 128) * sizeof(double))));
+      attr = true;
+    }
+    vec::k_dcgs_dots<128><<<grid, 128, sm2, st>>>(S, k, V, ldv, z, partial, 2 * kLdc + 8, out, 0, counters);
+  }
+  count_launch();
+  CPM_CUDA(cudaGetLastError());
+  return CPM_OK;
+}
+
+int launch_dcgs_update(const vec::Seg& S, int k, double* V, int64_t ldv, const double* z,
+                       const double* coef, cudaStream_t st) {
+  const int grid = S.nseg * S.gps;
+  if (k <= 64) {
+    const size_t sm = ((size_t)k * (256 + 4) + 2 * (size_t)k) * sizeof(double);
+    static bool attr = false;
+    if (!attr) {
+      CPM_CUDA(cudaFuncSetAttribute(vec::k_dcgs_update<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)(((size_t)64 * 260 + 128) * sizeof(double))));
+      attr = true;
+    }
+    vec::k_dcgs_update<256><<<grid, 256, sm, st>>>(S, k, V, ldv, z, coef, kLdc);
+  } else {
+    const size_t sm = ((size_t)k * (128 + 4) + 2 * (size_t)k) * sizeof(double);
+    static bool attr = false;
+    if (!attr) {
+      CPM_CUDA(cudaFuncSetAttribute(vec::k_dcgs_update<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)(((size_t)(kMaxRestart + 1) * 132 + 2 * (kMaxRestart + 1)) * sizeof(double))));
+      attr = true;
+    }
+    vec::k_dcgs_update<128><<<grid, 128, sm, st>>>(S, k, V, ldv, z, coef, kLdc);
+  }
+  count_launch();
+  CPM_CUDA(cudaGetLastError());
+  return CPM_OK;
+}
+}  // namespace
+
+namespace {
 
 // ---------------------------------------------------------------- scalar kernels (1 thread)
 __global__ void k_cycle_init(GState* st) {
@@ -136,6 +201,104 @@ __global__ void k_arnoldi_step(GState* st, int j, int m) {
   st->sc[j + 1] = nrm > 0.0 ? 1.0 / nrm : 0.0;
   st->breakdown = brk;
   if (st->est <= st->target || brk || j + 1 == m) st->done = 1;
+}
+
+// Delayed CGS2 step j (one thread).  Inputs (st->red, from k_dcgs_dots over the
+// columns Q_0..Q_{j-1}, u_j and the vectors u_j, z = A u_j):
+//   b = Q^T u_j, alpha = u_j.u_j, d = Q^T z, gamma = u_j.z.
+// u_j = rho q_j + Q b with rho^2 = alpha - |b|^2 (Pythagoras), so the pending
+// Hessenberg column j-1 is [cpend + b; rho] (finalised here: Givens, residual
+// estimate, convergence), and A q_j = (z - Q_{<=j} g)/rho with g = Hr b, so the
+// first projection of A q_j is cpend = ([d; rho mu] - g)/rho, mu = (gamma - b.d)/rho^2,
+// and the next lagged vector u_{j+1} = (z - mu u_j - Q (d - mu b))/rho
+// (k_dcgs_update, coefficients in st->coef).
+constexpr int kStepThreads = 128;
+__global__ void __launch_bounds__(kStepThreads) k_dcgs_step(GState* st, int j, int m) {
+  const int ld = kMaxRestart + 1, k = j + 1, tid = threadIdx.x;
+  const double* b = st->red;
+  const double* d = st->red + k;
+  __shared__ double sbb[kStepThreads / 32], sbd[kStepThreads / 32];
+  __shared__ int sdone;
+  double pbb = 0.0, pbd = 0.0;
+  for (int i = tid; i < j; i += kStepThreads) {
+    pbb += b[i] * b[i];
+    pbd += b[i] * d[i];
+  }
+  pbb = vec::warp_sum(pbb);
+  pbd = vec::warp_sum(pbd);
+  if ((tid & 31) == 0) {
+    sbb[tid >> 5] = pbb;
+    sbd[tid >> 5] = pbd;
+  }
+  __syncthreads();
+  double bb = 0.0, bd = 0.0;
+  for (int w = 0; w < kStepThreads / 32; ++w) {
+    bb += sbb[w];
+    bd += sbd[w];
+  }
+  const double alpha = st->red[j], gamma = st->red[k + j];
+  const double rho2 = alpha - bb;
+  const int brk = !(rho2 > 1e-28 * alpha);
+  const double rho = brk ? 0.0 : sqrt(rho2);
+  if (j >= 1)
+    for (int i = tid; i < j; i += kStepThreads) st->Hr[(size_t)(j - 1) * ld + i] = st->cpend[i] + b[i];
+  __syncthreads();
+  if (tid == 0) {
+    sdone = 0;
+    if (j == 0) {
+      st->g[0] *= rho;  // u_0 = r / beta: r = (beta rho) q_0
+      st->est = fabs(st->g[0]);
+      if (brk) sdone = 1;
+    } else {
+      double* Hr = st->Hr + (size_t)(j - 1) * ld;
+      double* H = st->H + (size_t)(j - 1) * ld;
+      Hr[j] = rho;
+      for (int i = 0; i <= j; ++i) H[i] = Hr[i];
+      const int c = j - 1;  // column index
+      for (int i = 0; i < c; ++i) {
+        const double t = st->cs[i] * H[i] + st->sn[i] * H[i + 1];
+        H[i + 1] = -st->sn[i] * H[i] + st->cs[i] * H[i + 1];
+        H[i] = t;
+      }
+      const double den = hypot(H[c], H[c + 1]);
+      if (den == 0.0) {
+        st->cs[c] = 1.0;
+        st->sn[c] = 0.0;
+      } else {
+        st->cs[c] = H[c] / den;
+        st->sn[c] = H[c + 1] / den;
+      }
+      H[c] = st->cs[c] * H[c] + st->sn[c] * H[c + 1];
+      H[c + 1] = 0.0;
+      st->g[c + 1] = -st->sn[c] * st->g[c];
+      st->g[c] = st->cs[c] * st->g[c];
+      st->est = fabs(st->g[c + 1]);
+      st->k = j;
+      st->its += 1;
+      st->breakdown = brk;
+      if (st->est <= st->target || brk || j == m) sdone = 1;
+    }
+    if (sdone) st->done = 1;
+  }
+  __syncthreads();
+  if (sdone) return;
+  const double mu = (gamma - bd) / rho2;
+  double* cb = st->coef;
+  double* ce = st->coef + (kMaxRestart + 2);
+  for (int l = tid; l <= j; l += kStepThreads) {
+    double gl = 0.0;  // (Hr b)_l, Hr[l, i] = 0 for l > i + 1
+    for (int i = (l > 0 ? l - 1 : 0); i < j; ++i) gl += st->Hr[(size_t)i * ld + l] * b[i];
+    const double ql = l < j ? d[l] : rho * mu;
+    st->cpend[l] = (ql - gl) / rho;
+  }
+  for (int i = tid; i < j; i += kStepThreads) {
+    cb[i] = b[i];
+    ce[i] = d[i] - mu * b[i];
+  }
+  if (tid == 0) {
+    st->coef[2 * (kMaxRestart + 2)] = rho;
+    st->coef[2 * (kMaxRestart + 2) + 1] = mu;
+  }
 }
 
 // Back substitution H(0:k,0:k) y = g(0:k), one warp (lanes split the row sums).
@@ -269,6 +432,36 @@ int gmres_device(const LinOp& A, const PrecOp* M, const double* b, double* x, in
     }
     if (its >= maxit) break;
     ++cycles;
+    if (!flex && !g_force_cgs2) {
+      // delayed CGS2: V_0 = r / beta is the first lagged vector
+      {
+        ProfScope ps(K_AXPY, s);
+        vec::k_scale<<<G, VB, 0, s>>>(S, ws.V, st->sc, 0, 0, ws.V);
+        count_launch();
+      }
+      for (int j = 0; j <= m; ++j) {
+        double* Vj = ws.V + (size_t)j * ws.ldv;
+        if (j < m) CPM_TRY(A.apply(Vj, ws.w, nullptr, s));  // z = A u_j
+        const int k = j + 1;
+        {
+          ProfScope ps(K_MDOT, s);
+          CPM_TRY(launch_dcgs_dots(S, k, ws.V, ws.ldv, ws.w, ws.partial, st->red, cnt + 1, s));
+          CPM_TRY(allreduce(st->red, 2 * k));
+        }
+        {
+          ProfScope ps(K_OTHER, s);
+          k_dcgs_step<<<1, kStepThreads, 0, s>>>(st, j, m);
+          count_launch();
+        }
+        CPM_TRY(fetch_state(ws, s));
+        its = ws.hst->its;
+        if (ws.hst->done || its >= maxit) break;
+        {
+          ProfScope ps(K_CGS_UPDATE, s);
+          CPM_TRY(launch_dcgs_update(S, k, ws.V, ws.ldv, ws.w, st->coef, s));
+        }
+      }
+    } else
     for (int j = 0; j < m; ++j) {
       double* Vj = ws.V + (size_t)j * ws.ldv;
       if (flex) {
@@ -315,7 +508,8 @@ int gmres_device(const LinOp& A, const PrecOp* M, const double* b, double* x, in
       ProfScope ps(K_AXPY, s);
       k_lsq<<<1, 32, 0, s>>>(st);
       count_launch();
-      vec::k_combine<<<G, VB, 0, s>>>(S, flex ? ws.Z : ws.V, ws.ldv, st->y, 0, flex ? nullptr : st->sc, 0,
+      const bool scaled = !flex && g_force_cgs2;  // CGS2 keeps the basis unnormalised
+      vec::k_combine<<<G, VB, 0, s>>>(S, flex ? ws.Z : ws.V, ws.ldv, st->y, 0, scaled ? st->sc : nullptr, 0,
                                       &st->k, 0, 0, nullptr, nullptr, nullptr, x, 1);
       count_launch();
     }

@@ -24,6 +24,11 @@ struct GState {
   int k, done, breakdown, its;                // contiguous: copied to the host together
   double est, beta2;                          // contiguous
   unsigned counter[8];
+  // delayed CGS2 (unpreconditioned GMRES)
+  double Hr[(kMaxRestart + 1) * kMaxRestart];  // unrotated Hessenberg columns
+  double cpend[kMaxRestart + 2];              // first projection of the pending column
+  double red[2 * (kMaxRestart + 2)];          // [<Q_i,u_j>, <u_j,u_j>] then [<Q_i,z>, <u_j,z>]
+  double coef[2 * (kMaxRestart + 2) + 2];     // b, e (stride kMaxRestart + 2), rho, mu
 };
 
 struct HostState {

@@ -251,6 +251,125 @@ static __global__ void __launch_bounds__(TB) k_proj(Seg S, int k, const double* 
   if (tid == 0) counters[s] = 0u;
 }
 
+// ---------------------------------------------------------------- DCGS2 passes
+// Delayed CGS2 (krylov.cu): per Arnoldi step one reduction pass and one update
+// pass over the basis.  Columns staged per tile: Q_0 .. Q_{j-1} and the lagged
+// vector u_j = V_j (k = j + 1 columns); z = A u_j streamed alongside.
+//   k_dcgs_dots:   out[i] = <col_i, u_j>,  out[k + i] = <col_i, z>   (i < k)
+//   k_dcgs_update: V_j <- (u_j - sum_i b_i Q_i) / rho
+//                  V_{j+1} <- (z - mu u_j - sum_i e_i Q_i) / rho
+//   (b = coef[0..j), e = coef[ldc .. ldc + j), rho = coef[2 ldc], mu = coef[2 ldc + 1])
+template <int TB>
+static __global__ void __launch_bounds__(TB) k_dcgs_dots(Seg S, int k, const double* __restrict__ V,
+                                                         int64_t ldv, const double* __restrict__ z,
+                                                         double* partial, int pld, double* out,
+                                                         int ldo, unsigned* counters) {
+  constexpr int SV = TB + 4;
+  extern __shared__ double smp[];
+  double* sv = smp;             // k columns of SV
+  double* sz = sv + (size_t)k * SV;
+  __shared__ bool last;
+  const int s = blockIdx.x / S.gps, lb = blockIdx.x % S.gps;
+  const int64_t o0 = S.off[s], n = S.off[s + 1] - o0;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  int kp = 8;
+  while (kp < k) kp <<= 1;
+  const int P = kp >= TB ? 1 : TB / kp;
+  const int col = tid / P, sub = tid % P;
+  const double* su = sv + (size_t)(k - 1) * SV;  // the lagged vector is the last column
+  double a1 = 0.0, a2 = 0.0;
+  for (int64_t t0 = (int64_t)lb * TB; t0 < n; t0 += (int64_t)S.gps * TB) {
+    const int64_t e = t0 + tid;
+    const bool in = e < n;
+    if (in) {
+      const double* p = V + o0 + e;
+      for (int i = 0; i < k; ++i) cpa8(sv + (size_t)i * SV + tid, p + (size_t)i * ldv);
+    }
+    cp_commit_v();
+    const double zv = in ? z[o0 + e] : 0.0;
+    cp_wait_all_v();
+    if (!in)
+      for (int i = 0; i < k; ++i) sv[(size_t)i * SV + tid] = 0.0;
+    sz[tid] = zv;
+    __syncthreads();
+    if (col < k) {
+      const double* c = sv + (size_t)col * SV;
+      for (int q = sub; q < TB; q += P) {
+        const double cv = c[q];
+        a1 += cv * su[q];
+        a2 += cv * sz[q];
+      }
+    }
+    __syncthreads();
+  }
+  for (int o = P >> 1; o > 0; o >>= 1) {
+    a1 += __shfl_xor_sync(0xffffffffu, a1, o);
+    a2 += __shfl_xor_sync(0xffffffffu, a2, o);
+  }
+  if (sub == 0 && col < k) {
+    partial[(size_t)blockIdx.x * pld + col] = a1;
+    partial[(size_t)blockIdx.x * pld + k + col] = a2;
+  }
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) last = (atomicAdd(counters + s, 1u) == (unsigned)S.gps - 1u);
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  for (int i = warp; i < 2 * k; i += TB / 32) {
+    const double a = partial_sum(partial, (size_t)s * S.gps, pld, S.gps, i, lane);
+    if (lane == 0) out[(size_t)s * ldo + i] = a;
+  }
+  if (tid == 0) counters[s] = 0u;
+}
+
+template <int TB>
+static __global__ void __launch_bounds__(TB) k_dcgs_update(Seg S, int k, double* V, int64_t ldv,
+                                                           const double* __restrict__ z,
+                                                           const double* __restrict__ coef, int ldc) {
+  constexpr int SV = TB + 4;
+  extern __shared__ double smp[];
+  double* sv = smp;             // k columns of SV
+  double* cb = sv + (size_t)k * SV;
+  double* ce = cb + k;
+  const int s = blockIdx.x / S.gps, lb = blockIdx.x % S.gps;
+  const int64_t o0 = S.off[s], n = S.off[s + 1] - o0;
+  const int tid = threadIdx.x;
+  const int j = k - 1;
+  for (int i = tid; i < j; i += TB) {
+    cb[i] = coef[i];
+    ce[i] = coef[ldc + i];
+  }
+  const double rinv = 1.0 / coef[2 * ldc], mu = coef[2 * ldc + 1];
+  __syncthreads();
+  for (int64_t t0 = (int64_t)lb * TB; t0 < n; t0 += (int64_t)S.gps * TB) {
+    const int64_t e = t0 + tid;
+    if (e >= n) continue;
+    const double* p = V + o0 + e;
+    for (int i = 0; i < k; ++i) cpa8(sv + (size_t)i * SV + tid, p + (size_t)i * ldv);
+    cp_commit_v();
+    const double zv = z[o0 + e];
+    cp_wait_all_v();
+    double sb0 = 0.0, sb1 = 0.0, se0 = 0.0, se1 = 0.0;
+    int i = 0;
+    for (; i + 1 < j; i += 2) {
+      const double q0 = sv[(size_t)i * SV + tid], q1 = sv[(size_t)(i + 1) * SV + tid];
+      sb0 += cb[i] * q0;
+      sb1 += cb[i + 1] * q1;
+      se0 += ce[i] * q0;
+      se1 += ce[i + 1] * q1;
+    }
+    if (i < j) {
+      const double q0 = sv[(size_t)i * SV + tid];
+      sb0 += cb[i] * q0;
+      se0 += ce[i] * q0;
+    }
+    const double uv = sv[(size_t)j * SV + tid];
+    V[(size_t)j * ldv + o0 + e] = (uv - (sb0 + sb1)) * rinv;
+    V[(size_t)(j + 1) * ldv + o0 + e] = (zv - mu * uv - (se0 + se1)) * rinv;
+  }
+}
+
 template <int TB>
 inline size_t proj_smem(int k) {
   return ((size_t)k * (TB + 4) + TB + (size_t)k + TB / 32) * sizeof(double);
