@@ -101,6 +101,19 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(self.rows)}
 
 
+KERNELS = ["extend", "laplace", "mdot", "cgs_update", "cgs_final", "axpy", "other"]
+
+
+def _traffic():
+    """ncu DRAM bytes (read + write) per apply, from the committed capture summary."""
+    p = os.path.join(ROOT, "profiles", "r01_traffic.json")
+    try:
+        d = json.load(open(p))
+        return float(d["apply_dram_bytes"])
+    except Exception:
+        return None
+
+
 def _dist():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -208,8 +221,20 @@ def run_mine(args):
     x = torch.zeros_like(u)
     c = CFG["c"]
 
+    prof = {"apply": {}, "solve": {}}
+
+    def take_profile(phase):
+        for k in KERNELS:
+            ms, n = cpm.cpm_profile_read(k)
+            a, b = prof[phase].get(k, (0.0, 0))
+            prof[phase][k] = (a + ms, b + n)
+        cpm.cpm_profile_reset()
+
     def step(record):
         evs = []
+        if record is not None:
+            cpm.cpm_profile_reset()
+            cpm.cpm_profile_enable(True)
         for _ in range(CFG["applies"]):
             a = torch.cuda.Event(enable_timing=True)
             b = torch.cuda.Event(enable_timing=True)
@@ -217,6 +242,8 @@ def run_mine(args):
             cpm.cpm_apply(band, c, u, y)
             b.record(stream)
             evs.append((a, b))
+        if record is not None:
+            take_profile("apply")
         x.zero_()
         sa = torch.cuda.Event(enable_timing=True)
         sb = torch.cuda.Event(enable_timing=True)
@@ -224,6 +251,8 @@ def run_mine(args):
         st = cpm.cpm_solve(band, c, f, x, rtol=CFG["rtol"], restart=CFG["restart"])
         sb.record(stream)
         if record is not None:
+            take_profile("solve")
+            cpm.cpm_profile_enable(False)
             record.append((evs, (sa, sb), st))
 
     for _ in range(args.warmup):
@@ -232,8 +261,6 @@ def run_mine(args):
 
     clocks = ClockSampler(local)
     clocks.start()
-    cpm.cpm_profile_reset()
-    cpm.cpm_profile_enable(True)
     launches0 = cpm.cpm_kernel_launches()
     rec = []
     if ws > 1:
@@ -249,15 +276,13 @@ def run_mine(args):
     if ws > 1:
         torch.distributed.barrier()
     launches = cpm.cpm_kernel_launches() - launches0
-    cpm.cpm_profile_enable(False)
     clk = clocks.stop()
     total_ms = ga.elapsed_time(gb)
     apply_ms = sum(a.elapsed_time(b) for evs, _, _ in rec for a, b in evs)
     solve_ms = [sa.elapsed_time(sb) for _, (sa, sb), _ in rec]
     stats = [st for _, _, st in rec]
-    ext_ms, ext_n = cpm.cpm_profile_read("extend")
-    lap_ms, lap_n = cpm.cpm_profile_read("laplace")
-    kern = {k: cpm.cpm_profile_read(k) for k in ["mdot", "cgs_update", "cgs_final", "axpy", "other"]}
+    ext_ms, ext_n = prof["apply"]["extend"]
+    lap_ms, lap_n = prof["apply"]["laplace"]
 
     # e2e: same metric through the C ABI with HOST buffers (pinned), copies inside the timed region
     y_host = torch.empty(nA, dtype=torch.float64).pin_memory()
@@ -283,9 +308,23 @@ def run_mine(args):
     e2e_value = ws * nA * CFG["applies"] * e2e_steps / e2e_s
 
     peak, peak_src = _peaks()
-    alg_bytes = 16 * nA + 28 * nE          # DESIGN.md §Roofline: u + y + (t_xyz + eoff) per eval node
+    alg_bytes = 16 * nA + 28 * nE          # DESIGN.md §Kernels: u + y + (t_xyz + eoff) per eval node
     mean_apply_s = (ext_ms + lap_ms) / 1e3 / max(ext_n, 1)
     achieved = alg_bytes / mean_apply_s / 1e9
+    traffic = _traffic()
+    # Krylov passes of the solve (delayed CGS2): per Arnoldi step j one reduction
+    # pass (reads V_0..V_j and z: (j + 2) * 8 n bytes) and one update pass (reads the
+    # same, writes q_j and u_{j+1}: (j + 4) * 8 n bytes); steps j = 0 .. per cycle
+    st_last = stats[-1]
+    kry_bytes = 0
+    left, m = st_last.iterations, CFG["restart"]
+    while left > 0:
+        steps = min(left, m)
+        for j in range(steps + 1):          # + the final reduction of the cycle
+            kry_bytes += 8 * nA * ((j + 2) + ((j + 4) if j < steps else 0))
+        left -= steps
+    kry_ms = sum(prof["solve"][k][0] for k in ("mdot", "cgs_update", "cgs_final")) / args.steps
+    kry_gbs = kry_bytes / (kry_ms / 1e3) / 1e9 if kry_ms > 0 else None
     if rank == 0:
         cpu_rate, cpu_s, cores = (None, None, None)
         if not args.no_cpu and ws == 1:
@@ -302,12 +341,20 @@ def run_mine(args):
             "solve": {"seconds_median": solve_med_ms / 1e3, "iterations": stats[-1].iterations,
                       "converged": stats[-1].converged, "resid_true_rel": stats[-1].resid_true / stats[-1].bnorm},
             "build_band_s": build_s,
-            "roofline": {"kernel": "apply = extend + laplace (per apply)", "bound": "hbm",
-                         "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": None, "peak_source": peak_src,
+            "roofline": {"kernel": "apply = k_extend_nt + k_laplace (one apply, the metric's unit)",
+                         "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                          "alg_bytes_per_apply": alg_bytes,
-                         "extend_ms": ext_ms / max(ext_n, 1), "laplace_ms": lap_ms / max(lap_n, 1)},
-            "kernels_ms_total": {"extend": ext_ms, "laplace": lap_ms, **{k: v[0] for k, v in kern.items()}},
+                         "extend_ms": ext_ms / max(ext_n, 1), "laplace_ms": lap_ms / max(lap_n, 1),
+                         "note": "extend is bound by shared-memory gathers (DESIGN.md §Kernels); "
+                                 "traffic = ncu DRAM bytes per apply (profiles/r01_traffic.json)"},
+            "roofline_solve": {"kernel": "Krylov passes of the solve (k_dcgs_dots + k_dcgs_update), "
+                                         "the largest share of a step",
+                               "bound": "hbm", "achieved": kry_gbs, "peak": peak, "unit": "GB/s",
+                               "frac": (kry_gbs / peak) if kry_gbs else None,
+                               "alg_bytes_per_solve": kry_bytes, "ms_per_solve": kry_ms},
+            "kernels_ms_per_step": {ph: {k: v[0] / args.steps for k, v in d.items() if v[1]}
+                                    for ph, d in prof.items()},
             "cpu_baseline": ({"value": cpu_rate, "unit": UNIT, "cores": cores, "kind": "oracle",
                               "sample": f"{args.cpu_rows} sampled active rows of config 1, "
                                         f"oracle.operator.apply_rows, {cpu_s:.1f} s"}
