@@ -359,3 +359,53 @@ def test_ras_fgmres_converges_to_single_domain_solution():
         x1, s1 = gmres(lambda v: A @ v, f, restart=30, rtol=1e-10, M=M)
         assert s1.converged
         assert np.abs(x1 - x0).max() / np.abs(x0).max() < 1e-8
+
+
+# ---------------------------------------------------------------- Schnakenberg IMEX (config 4)
+from oracle.reaction import SchnakenbergParams, imex_step, initial_state, reaction  # noqa: E402
+
+
+def test_schnakenberg_constant_state_is_scalar_euler():
+    """Spatially constant data: Delta_S^h kills constants, so one IMEX step is the
+    explicit Euler step of the kinetics ODE, u1 = u0 + dt gamma (a - u0 + u0^2 v0),
+    v1 = v0 + dt gamma (b - u0^2 v0) (hand formula, not the oracle's)."""
+    p = SchnakenbergParams()
+    b = Band(Sphere(1.0), 0.15)
+    u0, v0 = 0.7, 1.3
+    u1, v1 = imex_step(b, np.full(b.nA, u0), np.full(b.nA, v0), p)
+    eu = u0 + p.dt * p.gamma * (p.a - u0 + u0 * u0 * v0)
+    ev = v0 + p.dt * p.gamma * (p.b - u0 * u0 * v0)
+    assert np.abs(u1 - eu).max() <= 1e-10 and np.abs(v1 - ev).max() <= 1e-10
+
+
+def test_schnakenberg_steady_state_is_fixed_point():
+    """(a + b, b / (a + b)^2) zeroes both reaction terms: a step leaves it unchanged."""
+    p = SchnakenbergParams()
+    us, vs = p.a + p.b, p.b / (p.a + p.b) ** 2
+    ru, rv = reaction(np.array([us]), np.array([vs]), p)
+    assert abs(ru[0]) < 1e-14 and abs(rv[0]) < 1e-14
+    b = Band(Sphere(1.0), 0.15)
+    u1, v1 = imex_step(b, np.full(b.nA, us), np.full(b.nA, vs), p)
+    assert np.abs(u1 - us).max() <= 1e-10 and np.abs(v1 - vs).max() <= 1e-10
+
+
+def test_schnakenberg_pure_diffusion_eigenfunction():
+    """gamma = 0, u0 = Y_2^1(cp): backward Euler multiplies by 1 / (1 + dt mu l(l+1))
+    (Delta_S Y = -l(l+1) Y on the unit sphere), up to the O(h^2) of Delta_S^h."""
+    p = SchnakenbergParams(gamma=0.0, mu1=1.0, mu2=2.0, dt=0.1)
+    errs = []
+    for h in (0.16, 0.1):
+        b = Band(Sphere(1.0), h)
+        Y = exact_sph(b, 2, 1)
+        u1, v1 = imex_step(b, Y, Y, p)
+        errs.append(max(np.abs(u1 - Y / (1 + 0.1 * 1.0 * 6)).max(), np.abs(v1 - Y / (1 + 0.1 * 2.0 * 6)).max()))
+    assert errs[1] < 1e-2 and errs[0] / errs[1] > 0.8 * (0.16 / 0.1) ** 2
+
+
+def test_schnakenberg_initial_state_recipe():
+    """u = a + b, v = b/(a+b)^2 plus 1e-2 U[-1,1] (seed 3): bounds and independence of u, v noise."""
+    p = SchnakenbergParams()
+    b = Band(Sphere(1.0), 0.15)
+    u, v = initial_state(b, p)
+    assert np.all(np.abs(u - 1.0) <= 1e-2) and np.all(np.abs(v - 0.9) <= 1e-2)
+    assert abs(np.corrcoef(u, v)[0, 1]) < 0.1
