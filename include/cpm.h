@@ -5,7 +5,7 @@
  * "A closest point method library for PDEs on surfaces with parallel domain
  * decomposition solvers and preconditioners" (arXiv:2110.06322), reproduced in
  * PAPER.md; "PAPER.md:N" below cites its line N.  DESIGN.md lists the readings
- * (R1..R12) taken where the paper is silent.
+ * (R1..R14) taken where the paper is silent.
  *
  * Conventions (all entry points):
  *  - Return CPM_OK (0) on success, a negative CPM_ERR_* code otherwise; the
@@ -205,6 +205,24 @@ int cpm_eval_sph(const cpm_band* band, int l, int m, double scale, double* out, 
  * array of nq rows (a, kx, ky, kz). */
 int cpm_eval_torus_rhs(const cpm_band* band, const double* coeffs, int nq, double* out,
                        void* stream);
+
+/* ---------------------------------------------------------------- reaction-diffusion (config 4)
+ * cpm_rd_step — one IMEX Euler step of the Schnakenberg system on the surface
+ * (BASELINE.json configs[4]; the paper's time-dependent examples treat diffusion
+ * implicitly and the nonlinear coupling explicitly):
+ *   u_t = mu1 Delta_S u + gamma (a - u + u^2 v),  v_t = mu2 Delta_S v + gamma (b - u^2 v)
+ *   (c_i I - Delta_S^h) w1 = c_i (w0 + dt R_w(u0, v0)),  c_i = 1/(dt mu_i)      (reading R14)
+ * i.e. two shifted solves of Eq. 2 (GMRES(restart), rtol, warm-started from w0).
+ * u, v: DEVICE arrays of nA doubles, updated in place.  su, sv: statistics of the
+ * two solves (may be NULL).  Synchronises `stream`.
+ * Errors: CPM_ERR_ARG (null / host pointers, dt or mu_i <= 0), those of cpm_solve. */
+typedef struct cpm_rd_params {
+  double a, b, gamma, mu1, mu2, dt;
+  double rtol;
+  int32_t restart, maxit;
+} cpm_rd_params;
+int cpm_rd_step(const cpm_band* band, const cpm_rd_params* params, double* u, double* v,
+                cpm_solve_stats* su, cpm_solve_stats* sv, void* stream);
 
 /* ---------------------------------------------------------------- profiling
  * When enabled, every kernel launched by the library on the caller's stream is

@@ -20,6 +20,7 @@ from .cpm import (  # noqa: F401
     cpm_profile_reset,
     cpm_ras_apply,
     cpm_ras_setup,
+    cpm_rd_step,
     cpm_solve,
     cpm_version,
     load_library,

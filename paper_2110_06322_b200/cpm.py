@@ -64,6 +64,12 @@ class _SolveStats(ctypes.Structure):
     ]
 
 
+class _RdParams(ctypes.Structure):
+    _fields_ = [("a", ctypes.c_double), ("b", ctypes.c_double), ("gamma", ctypes.c_double),
+                ("mu1", ctypes.c_double), ("mu2", ctypes.c_double), ("dt", ctypes.c_double),
+                ("rtol", ctypes.c_double), ("restart", ctypes.c_int32), ("maxit", ctypes.c_int32)]
+
+
 _vp = ctypes.c_void_p
 _SIGS = {
     "cpm_version": (ctypes.c_char_p, []),
@@ -100,6 +106,8 @@ _SIGS = {
     "cpm_part_solve": (ctypes.c_int, [_vp, _vp, ctypes.c_double, _vp, _vp, ctypes.c_double, ctypes.c_int,
                                       ctypes.c_int, ctypes.POINTER(_SolveStats), _vp]),
     "cpm_part_free": (None, [_vp]),
+    "cpm_rd_step": (ctypes.c_int, [_vp, ctypes.POINTER(_RdParams), _vp, _vp, ctypes.POINTER(_SolveStats),
+                                   ctypes.POINTER(_SolveStats), _vp]),
 }
 
 _lib = None
@@ -301,6 +309,21 @@ def cpm_ras_apply(ras: Ras, r, z, stream=None):
     pz, sz = _ptr_stream(z, ras.band.n, True)
     _check(load_library().cpm_ras_apply(ras.handle, pr, pz, stream or sr or sz), "cpm_ras_apply")
     return z
+
+
+def cpm_rd_step(band: Band, u, v, a: float = 0.1, b: float = 0.9, gamma: float = 10.0,
+                mu1: float = 1e-3, mu2: float = 1e-2, dt: float = 1e-3, rtol: float = 1e-10,
+                restart: int = 50, maxit: int = 100000, stream=None):
+    """One IMEX Euler step of the Schnakenberg system (config 4); u, v device tensors,
+    updated in place.  Returns the two SolveStats."""
+    pu, su = _ptr_stream(u, band.n, True)
+    pv, sv = _ptr_stream(v, band.n, True)
+    prm = _RdParams(a, b, gamma, mu1, mu2, dt, rtol, restart, maxit)
+    s1, s2 = _SolveStats(), _SolveStats()
+    _check(load_library().cpm_rd_step(band.handle, ctypes.byref(prm), pu, pv, ctypes.byref(s1),
+                                      ctypes.byref(s2), stream or su or sv), "cpm_rd_step")
+    return tuple(SolveStats(x.iterations, bool(x.converged), x.cycles, bool(x.breakdown), x.resid_est,
+                            x.resid_true, x.bnorm, x.seconds) for x in (s1, s2))
 
 
 def cpm_eval_sph(band: Band, l: int, m: int, scale: float, out, stream=None):

@@ -1,6 +1,7 @@
 // solve.cu — cpm_solve (north_star item 3) and the RAS entry points (item 4).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstring>
 
 #include "internal.cuh"
@@ -51,4 +52,56 @@ extern "C" int cpm_solve(const cpm_band* b, double c, const double* f, double* u
   cudaFree(df_);
   cudaFree(du_);
   return rc;
+}
+
+// ---------------------------------------------------------------- reaction-diffusion
+namespace {
+// ru = c1 (u + dt gamma (a - u + u^2 v)),  rv = c2 (v + dt gamma (b - u^2 v))   (reading R14)
+__global__ void k_rd_rhs(int64_t n, const double* __restrict__ u, const double* __restrict__ v,
+                         double a, double b, double gamma, double dt, double c1, double c2,
+                         double* __restrict__ ru, double* __restrict__ rv) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double ui = u[i], vi = v[i];
+    const double u2v = ui * ui * vi;
+    ru[i] = c1 * (ui + dt * (gamma * (a - ui + u2v)));
+    rv[i] = c2 * (vi + dt * (gamma * (b - u2v)));
+  }
+}
+}  // namespace
+
+extern "C" int cpm_rd_step(const cpm_band* b, const cpm_rd_params* p, double* u, double* v,
+                           cpm_solve_stats* su, cpm_solve_stats* sv, void* stream) {
+  if (!b || !p || !u || !v) return fail(CPM_ERR_ARG, "cpm_rd_step: null argument");
+  if (u == v) return fail(CPM_ERR_ARG, "cpm_rd_step: u and v must not alias");
+  if (!(p->dt > 0.0) || !(p->mu1 > 0.0) || !(p->mu2 > 0.0))
+    return fail(CPM_ERR_ARG, "cpm_rd_step: dt, mu1, mu2 must be > 0");
+  if (!is_device_ptr(u) || !is_device_ptr(v))
+    return fail(CPM_ERR_ARG, "cpm_rd_step: u and v must be device pointers");
+  cudaStream_t s = (cudaStream_t)stream;
+  cpm_band* mb = const_cast<cpm_band*>(b);
+  if (!mb->dstage0) {
+    CPM_CUDA(cudaMalloc(&mb->dstage0, sizeof(double) * std::max<int64_t>(b->nA, 1)));
+    CPM_CUDA(cudaMalloc(&mb->dstage1, sizeof(double) * std::max<int64_t>(b->nA, 1)));
+  }
+  const double c1 = 1.0 / (p->dt * p->mu1), c2 = 1.0 / (p->dt * p->mu2);
+  {
+    ProfScope ps(K_AXPY, s);
+    const int grid = (int)std::min<int64_t>((b->nA + 255) / 256, 148 * 8);
+    k_rd_rhs<<<std::max(grid, 1), 256, 0, s>>>(b->nA, u, v, p->a, p->b, p->gamma, p->dt, c1, c2,
+                                               mb->dstage0, mb->dstage1);
+    count_launch();
+    CPM_CUDA(cudaGetLastError());
+  }
+  cpm_solve_stats l1, l2;
+  for (int q = 0; q < 2; ++q) {
+    const double c = q == 0 ? c1 : c2;
+    LinOp A;
+    A.apply = [b, c](const double* x, double* y, const double* scale, cudaStream_t st) {
+      return apply_device(b, c, x, y, scale, 0, st);
+    };
+    CPM_TRY(gmres_device(A, nullptr, q == 0 ? mb->dstage0 : mb->dstage1, q == 0 ? u : v, b->nA, p->rtol,
+                         p->restart, p->maxit, band_ws(b), q == 0 ? (su ? su : &l1) : (sv ? sv : &l2), s));
+  }
+  return CPM_OK;
 }
