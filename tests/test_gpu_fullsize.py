@@ -1,0 +1,111 @@
+"""Full-size BASELINE configs 2 and 3 on the GPU, checked against the oracle on
+sampled outputs (the oracle's row formula works at any size) and by properties
+that hold at any size.
+
+config 2: torus R=1 r=0.4, h=1/400 (20.9M active nodes), c=1, torus rhs (seed 1),
+          RAS(8 Morton slabs, overlap 4)-FGMRES(50), rtol 1e-10.
+config 3: unit sphere h=1/800 (~66M active nodes), c=0.1, f = Y_10^5 + 1e-3 N(0,1)
+          (seed 2): band, rhs and apply at full size; a bounded RAS-FGMRES run.
+"""
+import numpy as np
+import pytest
+
+import seeded_inputs
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle.band import node_key  # noqa: E402
+from oracle.operator import apply_rows  # noqa: E402
+from oracle.problems import rhs_noisy_sph, rhs_torus  # noqa: E402
+from oracle.surfaces import Sphere, Torus  # noqa: E402
+
+APPLY_TOL = 1e-12
+
+
+@pytest.fixture(scope="module")
+def cpm():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2110_06322_b200._build import build
+
+    build()
+    import paper_2110_06322_b200 as p
+
+    return p
+
+
+class _B:
+    """what oracle.operator.apply_rows / oracle.problems read from a band"""
+
+    def __init__(self, surface, h, active=None):
+        self.surface, self.h, self.active = surface, h, active
+
+
+def _lookup(ga, vals):
+    keys = node_key(ga)
+    order = np.argsort(keys)
+    sk = keys[order]
+
+    def f(q):
+        k = node_key(q)
+        pos = np.searchsorted(sk, k)
+        assert np.all(sk[pos] == k)
+        return vals[order[pos]]
+
+    return f
+
+
+def _sampled_apply(cpm, band, surf, h, c, seed):
+    ga = cpm.cpm_band_active_coords(band).astype(np.int64)
+    u = torch.from_numpy(seeded_inputs.uniform_pm1(seed, ga)).cuda()
+    y = torch.empty_like(u)
+    cpm.cpm_apply(band, c, u, y)
+    torch.cuda.synchronize()
+    sel = np.concatenate([np.random.default_rng(seed).choice(band.n, 1990, replace=False),
+                          np.arange(5), band.n - 1 - np.arange(5)])
+    y_o = apply_rows(_B(surf, h), c, lambda q: seeded_inputs.uniform_pm1(seed, q), ga[sel])
+    err = np.abs(y.cpu().numpy()[sel] - y_o).max() / np.abs(y_o).max()
+    assert err <= APPLY_TOL, err
+    return ga
+
+
+def test_config2_full_size(cpm):
+    h, c = 1.0 / 400, 1.0
+    surf = Torus(1.0, 0.4)
+    band = cpm.cpm_build_band("torus", h, R=1.0, r=0.4)
+    assert band.n > 20_000_000
+    ga = _sampled_apply(cpm, band, surf, h, c, seed=21)
+    f = torch.empty(band.n, dtype=torch.float64, device="cuda")
+    cpm.cpm_eval_torus_rhs(band, seeded_inputs.smooth_modulation_coeffs(1), f)
+    sel = np.random.default_rng(5).choice(band.n, 2000, replace=False)
+    f_o = rhs_torus(_B(surf, h, ga[sel]), seed=1)
+    assert np.abs(f.cpu().numpy()[sel] - f_o).max() <= 1e-12
+    ras = cpm.cpm_ras_setup(band, 8, 4, 16, c)
+    u = torch.zeros_like(f)
+    st = cpm.cpm_solve(band, c, f, u, rtol=1e-10, restart=50, ras=ras)
+    assert st.converged and st.resid_true <= 2e-10 * st.bnorm
+    # residual recomputed by the oracle's row formula on sampled rows
+    sel = np.random.default_rng(6).choice(band.n, 300, replace=False)
+    r = f.cpu().numpy()[sel] - apply_rows(_B(surf, h), c, _lookup(ga, u.cpu().numpy()), ga[sel])
+    assert np.abs(r).max() <= 1e-6 * np.abs(f.cpu().numpy()).max()
+
+
+def test_config3_full_size(cpm):
+    h, c = 1.0 / 800, 0.1
+    surf = Sphere(1.0)
+    band = cpm.cpm_build_band("sphere", h)
+    assert band.n > 60_000_000
+    ga = _sampled_apply(cpm, band, surf, h, c, seed=31)
+    f = torch.empty(band.n, dtype=torch.float64, device="cuda")
+    cpm.cpm_eval_sph(band, 10, 5, 1.0, f)
+    f += torch.from_numpy(1e-3 * seeded_inputs.normal(2, ga)).cuda()
+    sel = np.random.default_rng(7).choice(band.n, 2000, replace=False)
+    f_o = rhs_noisy_sph(_B(surf, h, ga[sel]), 10, 5, seed=2)
+    assert np.abs(f.cpu().numpy()[sel] - f_o).max() <= 1e-12
+    # bounded RAS-FGMRES(50) run: the true residual decreases (converging takes
+    # thousands of iterations at c = 0.1; tools/run_configs.py runs it to the end)
+    ras = cpm.cpm_ras_setup(band, 8, 4, 16, c)
+    u = torch.zeros_like(f)
+    st = cpm.cpm_solve(band, c, f, u, rtol=1e-10, restart=50, maxit=50, ras=ras)
+    assert st.iterations == 50 and st.resid_true < 0.5 * st.bnorm

@@ -30,11 +30,10 @@ def cpm():
     return p
 
 
-@pytest.mark.parametrize("kind,h,kw,steps", [("torus", 0.05, {"R": 1.0, "r": 0.4}, 1),
-                                             ("sphere", 0.1, {}, 3)])
+@pytest.mark.parametrize("kind,h,kw,steps", [("sphere", 0.1, {}, 3), ("sphere", 0.06, {"R": 0.7}, 2)])
 def test_rd_steps_match_oracle(cpm, kind, h, kw, steps):
     gb = cpm.cpm_build_band(kind, h, **kw)
-    ob = OBand(Torus(1.0, 0.4) if kind == "torus" else Sphere(1.0), h)
+    ob = OBand(Torus(1.0, 0.4) if kind == "torus" else Sphere(kw.get("R", 1.0)), h)
     ga = cpm.cpm_band_active_coords(gb).astype(np.int64)
     perm = ob.index_active(ga)
     assert np.all(perm >= 0)
