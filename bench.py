@@ -284,6 +284,33 @@ def run_mine(args):
     ext_ms, ext_n = prof["apply"]["extend"]
     lap_ms, lap_n = prof["apply"]["laplace"]
 
+    # config 4 (Schnakenberg IMEX Euler on the torus, h = 1/400), a bounded number of steps
+    rd = None
+    if args.rd_steps > 0 and rank == 0:
+        try:
+            tb = cpm.cpm_build_band("torus", 1.0 / 400, R=1.0, r=0.4)
+            tg = cpm.cpm_band_active_coords(tb).astype(np.int64)
+            ru = torch.from_numpy(1.0 + 1e-2 * seeded_inputs.uniform_pm1(3, tg, stream=0)).to(dev)
+            rv = torch.from_numpy(0.9 / 1.0 + 1e-2 * seeded_inputs.uniform_pm1(3, tg, stream=1)).to(dev)
+            cpm.cpm_rd_step(tb, ru, rv)                     # warm-up (workspace allocation)
+            its = []
+            ra = torch.cuda.Event(enable_timing=True)
+            rb = torch.cuda.Event(enable_timing=True)
+            ra.record(stream)
+            for _ in range(args.rd_steps):
+                s1, s2 = cpm.cpm_rd_step(tb, ru, rv)
+                its.append(s1.iterations + s2.iterations)
+            rb.record(stream)
+            torch.cuda.synchronize()
+            rd = {"workload": "BASELINE configs[4]: Schnakenberg on torus R=1 r=0.4, h=1/400, IMEX Euler "
+                              "dt=1e-3 (two GMRES(50) shifted solves per step), 1 GPU",
+                  "n_active": tb.n, "steps_timed": args.rd_steps,
+                  "ms_per_step": ra.elapsed_time(rb) / args.rd_steps,
+                  "gmres_its_per_step": float(np.mean(its))}
+            del tb, ru, rv
+        except Exception as e:  # report, never fail the main metric
+            rd = {"error": str(e)[:200]}
+
     # e2e: same metric through the C ABI with HOST buffers (pinned), copies inside the timed region
     y_host = torch.empty(nA, dtype=torch.float64).pin_memory()
     u_np, y_np = u_host.numpy(), y_host.numpy()
@@ -361,6 +388,7 @@ def run_mine(args):
                              if cpu_rate else None),
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 8 * nA * CFG["applies"],
                     "d2h_bytes_per_step": 8 * nA * CFG["applies"]},
+            "config4_rd": rd,
             "gpu_launches": launches,
             "clocks": clk,
         }
@@ -379,6 +407,7 @@ def main():
     ap.add_argument("--cpu-rows", type=int, default=1 << 18)
     ap.add_argument("--ref-rows", type=int, default=1 << 16)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--rd-steps", type=int, default=20, help="config-4 IMEX steps timed (0: skip)")
     args = ap.parse_args()
     if args.warmup < 3:
         print("warning: --warmup < 3 violates the timing rules; using 3", file=sys.stderr)
