@@ -197,7 +197,7 @@ __global__ void __launch_bounds__(kLapThreads) k_laplace(const TileHdr* __restri
   const TileHdr* T = tiles + t;
   const int a0 = T->a0, a1 = T->a1;
   if (a0 == a1) return;
-  constexpr int kOut = kBrickCells / kLapThreads, kGat = (kBrickCells + 384 + kLapThreads - 1) / kLapThreads;
+  constexpr int kOut = kBrickCells / kLapThreads;
   // output nodes: up to kOut per thread
   int ac[kOut];
   double au[kOut];
@@ -209,29 +209,40 @@ __global__ void __launch_bounds__(kLapThreads) k_laplace(const TileHdr* __restri
       au[k] = __ldg(u + a);
     }
   }
-  // 512 own cells + 6 x 64 face cells of the neighbours
+  // own tile: vb slot r (coalesced) -> its cell = the r-th set bit of emask
+  const int ne = T->e1 - T->e0;
+  const double* vt = vb + (size_t)t * kBrickCells;
 #pragma unroll
-  for (int k = 0; k < kGat; ++k) {
-    const int q = tid + k * kLapThreads;
-    int src = -1, c = 0, h = 0;
-    if (q < kBrickCells) {
-      src = t;
-      c = q;
-      h = hidx(q & 7, (q >> 3) & 7, q >> 6);
-    } else if (q < kBrickCells + 384) {
-      const int f = (q - kBrickCells) >> 6, i = q & 7, j = (q >> 3) & 7;
-      src = T->nbr[f];
-      const int axis = f >> 1, plus = (f & 1) == 0;
-      const int in = plus ? 0 : 7;    // layer read in the neighbour
-      const int out = plus ? 8 : -1;  // halo layer written here
-      if (axis == 0) { c = in + 8 * i + 64 * j; h = hidx(out, i, j); }
-      else if (axis == 1) { c = i + 8 * in + 64 * j; h = hidx(i, out, j); }
-      else { c = i + 8 * j + 64 * in; h = hidx(i, j, out); }
+  for (int k = 0; k < kBrickCells / kLapThreads; ++k) {
+    const int r = tid + k * kLapThreads;
+    if (r < ne) {
+      int w = 0;  // last word with epre[w] <= r (epre non-decreasing)
+#pragma unroll
+      for (int st = 8; st > 0; st >>= 1)
+        if (w + st < 16 && T->epre[w + st] <= r) w += st;
+      const int c = 32 * w + (int)__fns(T->emask[w], 0u, r - T->epre[w] + 1);
+      E[hidx(c & 7, (c >> 3) & 7, c >> 6)] = vt[r];
     }
-    if (src >= 0) {
-      const TileHdr* S = tiles + src;
-      const uint32_t m = S->emask[c >> 5], bit = 1u << (c & 31);
-      if (m & bit) E[h] = vb[(size_t)src * kBrickCells + S->epre[c >> 5] + __popc(m & (bit - 1u))];
+  }
+  // 6 x 64 face cells of the neighbours (rank lookup in the neighbour's mask)
+#pragma unroll
+  for (int k = 0; k < (384 + kLapThreads - 1) / kLapThreads; ++k) {
+    const int q = tid + k * kLapThreads;
+    if (q < 384) {
+      const int f = q >> 6, i = q & 7, j = (q >> 3) & 7;
+      const int src = T->nbr[f];
+      if (src >= 0) {
+        const int axis = f >> 1, plus = (f & 1) == 0;
+        const int in = plus ? 0 : 7;    // layer read in the neighbour
+        const int out = plus ? 8 : -1;  // halo layer written here
+        int c, h;
+        if (axis == 0) { c = in + 8 * i + 64 * j; h = hidx(out, i, j); }
+        else if (axis == 1) { c = i + 8 * in + 64 * j; h = hidx(i, out, j); }
+        else { c = i + 8 * j + 64 * in; h = hidx(i, j, out); }
+        const TileHdr* S = tiles + src;
+        const uint32_t m = S->emask[c >> 5], bit = 1u << (c & 31);
+        if (m & bit) E[h] = vb[(size_t)src * kBrickCells + S->epre[c >> 5] + __popc(m & (bit - 1u))];
+      }
     }
   }
   __syncthreads();
