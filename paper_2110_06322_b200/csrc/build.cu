@@ -357,18 +357,22 @@ __global__ void __launch_bounds__(512) k_sort_tile(const TileHdr* tiles, double*
 }
 
 // ------------------------------------------------------------------ B6c
-// Half-warp order: k_extend_nt gives the tile's nodes 16 at a time to the lanes
-// of a half-warp, whose 8-byte shared-memory gathers are conflict-free when the
-// distinct stencil bases among the 16 fall in distinct banks (box offset mod 16;
-// lanes with the same base read the same address: a broadcast).  Greedy, from
-// the base-sorted order: a half-warp takes the next compatible nodes, and only
-// when none is left any remaining ones.  One CTA per tile, thread 0 plans.
-__global__ void __launch_bounds__(512) k_halfwarp_order(const TileHdr* tiles, double* tx, double* ty,
-                                                        double* tz, uint32_t* eoff) {
+// Warp order: k_extend_nt gives the tile's nodes 32 at a time to the lanes of a
+// warp.  An 8-byte shared-memory load of a warp costs ONE wavefront when every
+// adjacent lane pair (2i, 2i+1) reads the same double and the 16 pair addresses
+// fall in distinct bank pairs, two otherwise (measured, tools/micro/shfl_vs_lds.cu).
+// All 64 gathers of a node are its stencil base + a lane-independent row
+// offset, so: nodes of equal base are paired, pairs are dealt 16 to a warp with
+// box offsets that are distinct mod 16 or equal (greedy from the base-sorted
+// order; when no compatible pair is left, any); the unpaired nodes follow, dealt
+// 16 per half-warp by the same rule.
+// One CTA per tile, thread 0 plans.
+__global__ void __launch_bounds__(512) k_warp_order(const TileHdr* tiles, double* tx, double* ty,
+                                                    double* tz, uint32_t* eoff) {
   __shared__ double sv[3][512];
   __shared__ uint32_t so[512];
-  __shared__ uint16_t perm[512];
-  __shared__ uint8_t used[512];
+  __shared__ uint16_t perm[512], pfirst[256], single[512];
+  __shared__ uint8_t pused[512];
   const TileHdr T = tiles[blockIdx.x];
   const int n = T.e1 - T.e0, t = threadIdx.x;
   if (t < n) {
@@ -376,33 +380,78 @@ __global__ void __launch_bounds__(512) k_halfwarp_order(const TileHdr* tiles, do
     sv[1][t] = ty[T.e0 + t];
     sv[2][t] = tz[T.e0 + t];
     so[t] = eoff[T.e0 + t];
-    used[t] = 0;
   }
   __syncthreads();
   if (t == 0) {
-    int out = 0, first = 0;
-    while (out < n) {
+    int np = 0, ns = 0;
+    for (int i = 0; i < n;) {  // groups of equal base -> pairs + a singleton
+      int j = i + 1;
+      while (j < n && (so[j] & 0xffffu) == (so[i] & 0xffffu)) ++j;
+      int q = i;
+      for (; q + 1 < j; q += 2) {
+        pfirst[np] = (uint16_t)q;
+        pused[np] = 0;
+        ++np;
+      }
+      if (q < j) single[ns++] = (uint16_t)q;
+      i = j;
+    }
+    int out = 0, first = 0, left = np;
+    while (left > 0) {
       uint32_t res = 0;
-      uint16_t offs[16];
+      uint16_t toff[16];
       int taken = 0;
-      for (int i = first; i < n && taken < 16; ++i) {
-        if (used[i]) continue;
-        const uint32_t o = so[i] & 0xffffu;
-        bool ok = !((res >> (o & 15)) & 1u);
-        for (int q = 0; q < taken && !ok; ++q) ok = offs[q] == o;
+      for (int p = first; p < np && taken < 16; ++p) {
+        if (pused[p]) continue;
+        const uint32_t o = so[pfirst[p]] & 0xffffu, r = o & 15u;
+        bool ok = !((res >> r) & 1u);
+        for (int q = 0; q < taken && !ok; ++q) ok = toff[q] == o;  // same address: broadcast
         if (!ok) continue;
-        res |= 1u << (o & 15);
-        offs[taken++] = (uint16_t)o;
-        used[i] = 1;
-        perm[out++] = (uint16_t)i;
-      }
-      for (int i = first; i < n && taken < 16; ++i) {  // nothing compatible left
-        if (used[i]) continue;
-        used[i] = 1;
-        perm[out++] = (uint16_t)i;
+        res |= 1u << r;
+        toff[taken] = (uint16_t)o;
+        pused[p] = 1;
+        perm[out++] = pfirst[p];
+        perm[out++] = (uint16_t)(pfirst[p] + 1);
         ++taken;
+        --left;
       }
-      while (first < n && used[first]) ++first;
+      for (int p = first; p < np && taken < 16; ++p) {  // nothing compatible left
+        if (pused[p]) continue;
+        pused[p] = 1;
+        perm[out++] = pfirst[p];
+        perm[out++] = (uint16_t)(pfirst[p] + 1);
+        ++taken;
+        --left;
+      }
+      while (first < np && pused[first]) ++first;
+    }
+    // unpaired nodes: 16 per half-warp with distinct box offsets mod 16 (or equal)
+    for (int q = 0; q < ns; ++q) pused[q] = 0;  // reused as "dealt" flags (ns <= 256)
+    int sfirst = 0, sleft = ns;
+    while (sleft > 0) {
+      uint32_t res = 0;
+      uint16_t toff[16];
+      int taken = 0;
+      for (int q = sfirst; q < ns && taken < 16; ++q) {
+        if (pused[q]) continue;
+        const uint32_t o = so[single[q]] & 0xffffu, r = o & 15u;
+        bool ok = !((res >> r) & 1u);
+        for (int z = 0; z < taken && !ok; ++z) ok = toff[z] == o;
+        if (!ok) continue;
+        res |= 1u << r;
+        toff[taken++] = (uint16_t)o;
+        pused[q] = 1;
+        perm[out++] = single[q];
+        --sleft;
+      }
+      for (int q = sfirst; q < ns && taken < 16; ++q) {
+        if (pused[q]) continue;
+        pused[q] = 1;
+        perm[out++] = single[q];
+        ++taken;
+        --sleft;
+      }
+      while (sfirst < ns && pused[sfirst]) ++sfirst;
     }
   }
   __syncthreads();
@@ -793,8 +842,8 @@ int build_band(const cpm_surface* surf, double h, int p, double L, cudaStream_t 
   count_launch();
   CPM_CUDA(cudaGetLastError());
 
-  // B6c half-warp order
-  k_halfwarp_order<<<totT, 512, 0, s>>>(B->tiles, B->tx, B->ty, B->tz, B->eoff);
+  // B6c warp order (one-wavefront gathers)
+  k_warp_order<<<totT, 512, 0, s>>>(B->tiles, B->tx, B->ty, B->tz, B->eoff);
   count_launch();
   CPM_CUDA(cudaGetLastError());
 
