@@ -64,7 +64,7 @@ __device__ __forceinline__ void cp_wait() {
 // few distinct addresses (broadcast).  u is read with an evict-last L2 policy
 // and vb written with one, so both stay resident in L2 for k_laplace.
 constexpr int kNtThreads = 128;
-constexpr int kNtNodes = 4;  // eval nodes per tile <= 512 = 4 * kNtThreads
+constexpr int kNtPre = 3;  // slots per thread whose node offsets are prefetched
 
 __device__ __forceinline__ uint64_t policy_evict_last() {
   uint64_t p;
@@ -99,6 +99,42 @@ __device__ __forceinline__ void st_hint(double* p, double v, uint64_t pol) {
   asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;\n" ::"l"(p), "d"(v), "l"(pol) : "memory");
 }
 
+// Slot s of a tile (thread tid handles slots tid + 128 k): nodes 0 .. 2np-1 (equal-
+// base pairs, build.cu k_warp_order) one per slot; the unpaired nodes two slots
+// each (both lanes of a lane pair gather the same stencil, the even one writes),
+// so every adjacent lane pair of a warp reads one address: one-wavefront gathers.
+__device__ __forceinline__ int slot_node(int s, int np2, bool& write) {
+  if (s < np2) {
+    write = true;
+    return s;
+  }
+  write = ((s - np2) & 1) == 0;
+  return np2 + ((s - np2) >> 1);
+}
+
+__device__ __forceinline__ void contract_node(const double (&tn)[3], uint32_t eo,
+                                              const double* __restrict__ box, int sx, int sxy,
+                                              double* __restrict__ out, bool write, uint64_t pol) {
+  double wx[4], wy[4], wz[4];
+  lagrange4(tn[0], wx);
+  lagrange4(tn[1], wy);
+  lagrange4(tn[2], wz);
+  const double* p = box + (eo & 0xffffu);
+  double acc = 0.0;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    double accy = 0.0;
+#pragma unroll
+    for (int bb = 0; bb < 4; ++bb) {
+      const double* row = p + bb * sx + c * sxy;
+      const double rx = (wx[0] * row[0] + wx[1] * row[1]) + (wx[2] * row[2] + wx[3] * row[3]);
+      accy += wy[bb] * rx;
+    }
+    acc += wz[c] * accy;
+  }
+  if (write) st_hint(out + (eo >> 16), acc, pol);
+}
+
 template <bool ZERO>
 __global__ void __launch_bounds__(kNtThreads, 8)
     k_extend_nt(const TileHdr* __restrict__ tiles, int boxCells, int descCap,
@@ -112,18 +148,22 @@ __global__ void __launch_bounds__(kNtThreads, 8)
   const int t = blockIdx.x, tid = threadIdx.x;
   const TileHdr* T = tiles + t;
   const int e0 = T->e0, ne = T->e1 - e0, r0 = T->r0, r1 = T->r1;
+  const int np2 = 2 * T->np, nslot = 2 * ne - np2;
   const int sx = T->pad[0], sxy = T->pad[1];
   const uint64_t pfirst = policy_evict_first(), plast = policy_evict_last();
-  double nt[kNtNodes][3];
-  uint32_t eo[kNtNodes];
+  // the first kNtPre slots of this thread are requested before the box is staged
+  double nt[kNtPre][3];
+  uint32_t eo[kNtPre];
 #pragma unroll
-  for (int k = 0; k < kNtNodes; ++k) {
-    const int i = tid + k * kNtThreads;
-    if (i < ne) {
-      nt[k][0] = ld_hint(tx + e0 + i, pfirst);
-      nt[k][1] = ld_hint(ty + e0 + i, pfirst);
-      nt[k][2] = ld_hint(tz + e0 + i, pfirst);
-      eo[k] = ld_hint(eoff + e0 + i, pfirst);
+  for (int k = 0; k < kNtPre; ++k) {
+    const int sl = tid + k * kNtThreads;
+    if (sl < nslot) {
+      bool w;
+      const int i = e0 + slot_node(sl, np2, w);
+      nt[k][0] = ld_hint(tx + i, pfirst);
+      nt[k][1] = ld_hint(ty + i, pfirst);
+      nt[k][2] = ld_hint(tz + i, pfirst);
+      eo[k] = ld_hint(eoff + i, pfirst);
     }
   }
   if (ZERO) {
@@ -153,27 +193,19 @@ __global__ void __launch_bounds__(kNtThreads, 8)
   __syncthreads();
   double* out = vb + (size_t)t * kBrickCells;
 #pragma unroll
-  for (int k = 0; k < kNtNodes; ++k) {
-    if (tid + k * kNtThreads < ne) {
-      double wx[4], wy[4], wz[4];
-      lagrange4(nt[k][0], wx);
-      lagrange4(nt[k][1], wy);
-      lagrange4(nt[k][2], wz);
-      const double* p = box + (eo[k] & 0xffffu);
-      double acc = 0.0;
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        double accy = 0.0;
-#pragma unroll
-        for (int bb = 0; bb < 4; ++bb) {
-          const double* row = p + bb * sx + c * sxy;
-          const double rx = (wx[0] * row[0] + wx[1] * row[1]) + (wx[2] * row[2] + wx[3] * row[3]);
-          accy += wy[bb] * rx;
-        }
-        acc += wz[c] * accy;
-      }
-      st_hint(out + (eo[k] >> 16), acc, plast);
+  for (int k = 0; k < kNtPre; ++k) {
+    const int sl = tid + k * kNtThreads;
+    if (sl < nslot) {
+      bool w;
+      slot_node(sl, np2, w);
+      contract_node(nt[k], eo[k], box, sx, sxy, out, w, plast);
     }
+  }
+  for (int sl = tid + kNtPre * kNtThreads; sl < nslot; sl += kNtThreads) {
+    bool w;
+    const int i = e0 + slot_node(sl, np2, w);
+    double tn[3] = {ld_hint(tx + i, pfirst), ld_hint(ty + i, pfirst), ld_hint(tz + i, pfirst)};
+    contract_node(tn, ld_hint(eoff + i, pfirst), box, sx, sxy, out, w, plast);
   }
 }
 

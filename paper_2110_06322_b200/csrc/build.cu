@@ -367,12 +367,13 @@ __global__ void __launch_bounds__(512) k_sort_tile(const TileHdr* tiles, double*
 // order; when no compatible pair is left, any); the unpaired nodes follow, dealt
 // 16 per half-warp by the same rule.
 // One CTA per tile, thread 0 plans.
-__global__ void __launch_bounds__(512) k_warp_order(const TileHdr* tiles, double* tx, double* ty,
+__global__ void __launch_bounds__(512) k_warp_order(TileHdr* tiles, double* tx, double* ty,
                                                     double* tz, uint32_t* eoff) {
   __shared__ double sv[3][512];
   __shared__ uint32_t so[512];
   __shared__ uint16_t perm[512], pfirst[256], single[512];
   __shared__ uint8_t pused[512];
+  __shared__ int npair;
   const TileHdr T = tiles[blockIdx.x];
   const int n = T.e1 - T.e0, t = threadIdx.x;
   if (t < n) {
@@ -396,62 +397,41 @@ __global__ void __launch_bounds__(512) k_warp_order(const TileHdr* tiles, double
       if (q < j) single[ns++] = (uint16_t)q;
       i = j;
     }
-    int out = 0, first = 0, left = np;
-    while (left > 0) {
-      uint32_t res = 0;
-      uint16_t toff[16];
-      int taken = 0;
-      for (int p = first; p < np && taken < 16; ++p) {
-        if (pused[p]) continue;
-        const uint32_t o = so[pfirst[p]] & 0xffffu, r = o & 15u;
-        bool ok = !((res >> r) & 1u);
-        for (int q = 0; q < taken && !ok; ++q) ok = toff[q] == o;  // same address: broadcast
-        if (!ok) continue;
-        res |= 1u << r;
-        toff[taken] = (uint16_t)o;
-        pused[p] = 1;
-        perm[out++] = pfirst[p];
-        perm[out++] = (uint16_t)(pfirst[p] + 1);
-        ++taken;
-        --left;
+    npair = np;
+    // warps of 16 items (a pair, or an unpaired node on both lanes of a lane pair):
+    // pairs first, the warp in progress continues with the unpaired nodes
+    int out = 0, taken = 0;
+    uint32_t res = 0;
+    uint16_t toff[16];
+    for (int phase = 0; phase < 2; ++phase) {
+      const int m = phase == 0 ? np : ns;
+      for (int q = 0; q < m; ++q) pused[q] = 0;
+      int first = 0, left = m;
+      while (left > 0) {
+        for (int pass = 0; pass < 2 && taken < 16; ++pass) {  // compatible first, then any
+          for (int q = first; q < m && taken < 16; ++q) {
+            if (pused[q]) continue;
+            const int node = phase == 0 ? pfirst[q] : single[q];
+            const uint32_t o = so[node] & 0xffffu, r = o & 15u;
+            if (pass == 0) {
+              bool ok = !((res >> r) & 1u);
+              for (int z = 0; z < taken && !ok; ++z) ok = toff[z] == o;  // same address: broadcast
+              if (!ok) continue;
+            }
+            res |= 1u << r;
+            toff[taken++] = (uint16_t)o;
+            pused[q] = 1;
+            --left;
+            perm[out++] = (uint16_t)node;
+            if (phase == 0) perm[out++] = (uint16_t)(node + 1);
+          }
+        }
+        while (first < m && pused[first]) ++first;
+        if (taken == 16) {
+          taken = 0;
+          res = 0;
+        }
       }
-      for (int p = first; p < np && taken < 16; ++p) {  // nothing compatible left
-        if (pused[p]) continue;
-        pused[p] = 1;
-        perm[out++] = pfirst[p];
-        perm[out++] = (uint16_t)(pfirst[p] + 1);
-        ++taken;
-        --left;
-      }
-      while (first < np && pused[first]) ++first;
-    }
-    // unpaired nodes: 16 per half-warp with distinct box offsets mod 16 (or equal)
-    for (int q = 0; q < ns; ++q) pused[q] = 0;  // reused as "dealt" flags (ns <= 256)
-    int sfirst = 0, sleft = ns;
-    while (sleft > 0) {
-      uint32_t res = 0;
-      uint16_t toff[16];
-      int taken = 0;
-      for (int q = sfirst; q < ns && taken < 16; ++q) {
-        if (pused[q]) continue;
-        const uint32_t o = so[single[q]] & 0xffffu, r = o & 15u;
-        bool ok = !((res >> r) & 1u);
-        for (int z = 0; z < taken && !ok; ++z) ok = toff[z] == o;
-        if (!ok) continue;
-        res |= 1u << r;
-        toff[taken++] = (uint16_t)o;
-        pused[q] = 1;
-        perm[out++] = single[q];
-        --sleft;
-      }
-      for (int q = sfirst; q < ns && taken < 16; ++q) {
-        if (pused[q]) continue;
-        pused[q] = 1;
-        perm[out++] = single[q];
-        ++taken;
-        --sleft;
-      }
-      while (sfirst < ns && pused[sfirst]) ++sfirst;
     }
   }
   __syncthreads();
@@ -462,6 +442,7 @@ __global__ void __launch_bounds__(512) k_warp_order(const TileHdr* tiles, double
     tz[T.e0 + t] = sv[2][o];
     eoff[T.e0 + t] = so[o];
   }
+  if (t == 0) tiles[blockIdx.x].np = npair;
 }
 
 // ------------------------------------------------------------------ B7

@@ -47,7 +47,7 @@ struct ProfScope {
 void count_launch();
 
 // ------------------------------------------------------------------ band data
-// One tile = one occupied 8^3 brick.  64-bit aligned, 192 bytes.
+// One tile = one occupied 8^3 brick.  64-bit aligned, 200 bytes.
 // E u of the tile's eval nodes lives in vb[slot * 512 + rank], rank = position of
 // the node's brick cell among the set bits of emask (cell order), so a tile's
 // values are contiguous (compact) and any cell is located by a popcount.
@@ -62,8 +62,10 @@ struct TileHdr {
   int32_t pad[3];      // row stride, plane stride of the box; segment id (RAS)
   uint32_t emask[16];  // eval-node cells of the brick (Sigma_A u Sigma_G), bit = cell
   uint16_t epre[16];   // epre[w] = set bits of emask[0..w)
+  int32_t np;          // eval nodes e0 + 2p, e0 + 2p + 1 (p < np) share a stencil base
+  int32_t pad2;
 };
-static_assert(sizeof(TileHdr) == 192, "TileHdr layout");
+static_assert(sizeof(TileHdr) == 200, "TileHdr layout");
 
 __host__ __device__ inline int popc32(uint32_t v) {
 #ifdef __CUDA_ARCH__
