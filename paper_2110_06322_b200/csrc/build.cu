@@ -368,12 +368,13 @@ __global__ void __launch_bounds__(512) k_sort_tile(const TileHdr* tiles, double*
 // 16 per half-warp by the same rule.
 // One CTA per tile, thread 0 plans.
 __global__ void __launch_bounds__(512) k_warp_order(TileHdr* tiles, double* tx, double* ty,
-                                                    double* tz, uint32_t* eoff) {
+                                                    double* tz, uint32_t* eoff, int boxCap) {
   __shared__ double sv[3][512];
   __shared__ uint32_t so[512];
   __shared__ uint16_t perm[512], pfirst[256], single[512];
   __shared__ uint8_t pused[512];
   __shared__ int npair;
+  __shared__ unsigned long long best;
   const TileHdr T = tiles[blockIdx.x];
   const int n = T.e1 - T.e0, t = threadIdx.x;
   if (t < n) {
@@ -382,7 +383,53 @@ __global__ void __launch_bounds__(512) k_warp_order(TileHdr* tiles, double* tx, 
     sv[2][t] = tz[T.e0 + t];
     so[t] = eoff[T.e0 + t];
   }
+  if (t == 0) best = ~0ull;
   __syncthreads();
+  // Box strides for bank spread: the dealing below needs, per warp, 16 items with
+  // distinct stencil-base offsets mod 16, so choose the padded strides (row stride
+  // sx + a, plane stride (sx + a) sy + b, a, b < 16) that make the residues of the
+  // tile's distinct bases most uniform (largest minimum count, then the smallest
+  // box), among those no larger than the band's largest box.  Bases are decoded
+  // from the current offsets.
+  {
+    const int px0 = T.pad[0], pxy0 = T.pad[1];
+    const int a = t & 15, b = (t >> 4) & 15;
+    const int px = T.sx + a, pxy = px * T.sy + b;
+    int cnt[16];
+#pragma unroll
+    for (int r = 0; r < 16; ++r) cnt[r] = 0;
+    if (t < 256) {
+      for (int i = 0; i < n; ++i) {
+        const int o = so[i] & 0xffff;
+        if (i > 0 && o == (int)(so[i - 1] & 0xffff)) continue;  // distinct bases (sorted input)
+        const int dz = o / pxy0, rem = o - dz * pxy0, dy = rem / px0, dx = rem - dy * px0;
+        cnt[(dx + px * dy + pxy * dz) & 15]++;
+      }
+      int mn = 1 << 20;
+#pragma unroll
+      for (int r = 0; r < 16; ++r) mn = min(mn, cnt[r]);
+      const unsigned cells = (unsigned)(pxy * T.sz);
+      if (cells <= (unsigned)boxCap)  // never enlarge the band's largest box (smem per CTA)
+        atomicMin(&best, ((unsigned long long)(1023 - min(mn, 1023)) << 40) |
+                             ((unsigned long long)cells << 8) | (unsigned long long)t);
+    }
+  }
+  __syncthreads();
+  if (best != ~0ull) {
+    const int bt = (int)(best & 0xff);
+    const int px = T.sx + (bt & 15), pxy = px * T.sy + ((bt >> 4) & 15);
+    const int px0 = T.pad[0], pxy0 = T.pad[1];
+    if (t < n) {
+      const int o = so[t] & 0xffff;
+      const int dz = o / pxy0, rem = o - dz * pxy0, dy = rem / px0, dx = rem - dy * px0;
+      so[t] = (so[t] & 0xffff0000u) | (uint32_t)(dx + px * dy + pxy * dz);
+    }
+    __syncthreads();
+    if (t == 0) {
+      tiles[blockIdx.x].pad[0] = px;
+      tiles[blockIdx.x].pad[1] = pxy;
+    }
+  }
   if (t == 0) {
     int np = 0, ns = 0;
     for (int i = 0; i < n;) {  // groups of equal base -> pairs + a singleton
@@ -546,6 +593,11 @@ __global__ void k_round4(int nb, const int* ne, int* ne4) {
   int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b < nb) ne4[b] = (ne[b] + 3) & ~3;
   if (b == 0) ne4[nb] = 0;
+}
+
+__global__ void k_max_box(int nT, const TileHdr* tiles, int* mx) {
+  int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < nT) atomicMax(mx, tiles[t].pad[1] * tiles[t].sz);
 }
 
 __global__ void k_flags(int nb, const int* ne, int* flag) {
@@ -824,9 +876,18 @@ int build_band(const cpm_surface* surf, double h, int p, double L, cudaStream_t 
   CPM_CUDA(cudaGetLastError());
 
   // B6c warp order (one-wavefront gathers)
-  k_warp_order<<<totT, 512, 0, s>>>(B->tiles, B->tx, B->ty, B->tz, B->eoff);
+  k_warp_order<<<totT, 512, 0, s>>>(B->tiles, B->tx, B->ty, B->tz, B->eoff, B->maxBox);
   count_launch();
   CPM_CUDA(cudaGetLastError());
+  {  // the strides may have changed: largest box again
+    DevBuf mb;
+    CPM_TRY(dalloc<int>(mb, 1, "max box"));
+    CPM_CUDA(cudaMemsetAsync(mb.p, 0, sizeof(int), s));
+    k_max_box<<<grid_for(totT, 256), 256, 0, s>>>(totT, B->tiles, mb.as<int>());
+    count_launch();
+    CPM_CUDA(cudaMemcpyAsync(&B->maxBox, mb.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CPM_CUDA(cudaStreamSynchronize(s));
+  }
 
   // B7 fill runs
   DevBuf nrows, rowbase, rowcnt, runstart;
