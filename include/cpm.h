@@ -188,11 +188,41 @@ int cpm_part_apply_local(const cpm_part* part, double c, const double* u_owned,
 int cpm_part_apply(const cpm_part* part, const cpm_comm* comm, double c, const double* u_owned,
                    double* y_owned, void* stream);
 /* Distributed GMRES(restart) on the owned slices (conventions of cpm_solve); every
- * rank gets identical statistics. */
+ * rank gets identical statistics.  ras: NULL, or this rank's cpm_part_ras_setup
+ * preconditioner (flexible GMRES, RAS halo exchanged before every apply). */
 int cpm_part_solve(const cpm_part* part, const cpm_comm* comm, double c, const double* f_owned,
-                   double* u_owned, double rtol, int restart, int maxit, cpm_solve_stats* stats,
-                   void* stream);
+                   double* u_owned, double rtol, int restart, int maxit, const cpm_ras* ras,
+                   cpm_solve_stats* stats, void* stream);
 void cpm_part_free(cpm_part* part);
+
+/* ---------------------------------------------------------------- distributed RAS (items 4 + 5)
+ * cpm_part_ras_setup — this rank's share of the one-level RAS preconditioner of
+ * cpm_ras_setup for a partitioned band: n_sub Morton-slab subdomains (reading
+ * R8), n_sub a multiple of nranks (as in the paper), rank r handles
+ * subdomains [r n_sub/R, (r+1) n_sub/R) whose disjoint parts are exactly its
+ * owned slab.  The overlap (reading R7) reaches into other ranks' slabs: those
+ * members form the RAS HALO, received before every apply (cpm_ras_halo_nodes /
+ * cpm_ras_set_send, as for the operator halo); the inner solves and the
+ * restricted prolongation are rank-local.  Errors: CPM_ERR_ARG, CPM_ERR_CUDA. */
+typedef struct cpm_ras_info {
+  int32_t n_sub, sub0, n_sub_local, rank, nranks;
+  int64_t n_members;  /* concatenated overlapping subdomains of this rank */
+  int64_t n_owned, n_halo, n_send;
+} cpm_ras_info;
+int cpm_part_ras_setup(const cpm_part* part, int n_sub, int overlap, int k_inner, double c,
+                       void* stream, cpm_ras** out);
+int cpm_ras_get_info(const cpm_ras* ras, cpm_ras_info* info);
+/* Global band-order indices of the RAS halo, sorted (grouped by owner), HOST array. */
+int cpm_ras_halo_nodes(const cpm_ras* ras, int64_t* halo_host);
+/* What this rank sends to each peer's RAS halo (layout of cpm_part_set_send). */
+int cpm_ras_set_send(cpm_ras* ras, const int64_t* send_global_host, const int64_t* counts_host);
+/* z_owned = (M r)_owned with the RAS-halo values given explicitly (no communication);
+ * r_halo: n_halo doubles in cpm_ras_halo_nodes order.  Device pointers. */
+int cpm_part_ras_apply_local(const cpm_ras* ras, const double* r_owned, const double* r_halo,
+                             double* z_owned, void* stream);
+/* RAS-halo exchange over `comm` + local apply.  Device pointers (n_owned doubles). */
+int cpm_part_ras_apply(const cpm_ras* ras, const cpm_comm* comm, const double* r_owned,
+                       double* z_owned, void* stream);
 
 /* ---------------------------------------------------------------- problem data
  * cpm_eval_sph — out_i = scale * Y_l^m(cp(x_i)) on the active nodes, real

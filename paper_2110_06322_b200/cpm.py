@@ -104,7 +104,14 @@ _SIGS = {
     "cpm_part_apply_local": (ctypes.c_int, [_vp, ctypes.c_double, _vp, _vp, _vp, _vp]),
     "cpm_part_apply": (ctypes.c_int, [_vp, _vp, ctypes.c_double, _vp, _vp, _vp]),
     "cpm_part_solve": (ctypes.c_int, [_vp, _vp, ctypes.c_double, _vp, _vp, ctypes.c_double, ctypes.c_int,
-                                      ctypes.c_int, ctypes.POINTER(_SolveStats), _vp]),
+                                      ctypes.c_int, _vp, ctypes.POINTER(_SolveStats), _vp]),
+    "cpm_part_ras_setup": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_double,
+                                          _vp, ctypes.POINTER(_vp)]),
+    "cpm_ras_get_info": (ctypes.c_int, [_vp, _vp]),
+    "cpm_ras_halo_nodes": (ctypes.c_int, [_vp, _vp]),
+    "cpm_ras_set_send": (ctypes.c_int, [_vp, _vp, _vp]),
+    "cpm_part_ras_apply_local": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp]),
+    "cpm_part_ras_apply": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp]),
     "cpm_part_free": (None, [_vp]),
     "cpm_rd_step": (ctypes.c_int, [_vp, ctypes.POINTER(_RdParams), _vp, _vp, ctypes.POINTER(_SolveStats),
                                    ctypes.POINTER(_SolveStats), _vp]),
@@ -480,12 +487,70 @@ def cpm_part_apply(part: Part, comm: Comm, c: float, u_owned, y_owned, stream=No
 
 
 def cpm_part_solve(part: Part, comm: Comm, c: float, f_owned, u_owned, rtol: float = 1e-10,
-                   restart: int = 30, maxit: int = 100000, stream=None) -> SolveStats:
+                   restart: int = 30, maxit: int = 100000, ras=None, stream=None) -> SolveStats:
     pf, sf = _ptr_stream(f_owned, part.n_owned, False)
     pu, _ = _ptr_stream(u_owned, part.n_owned, True)
     st = _SolveStats()
     _check(load_library().cpm_part_solve(part.handle, comm.handle if comm else None, float(c), pf, pu,
-                                         float(rtol), int(restart), int(maxit), ctypes.byref(st), stream or sf),
-           "cpm_part_solve")
+                                         float(rtol), int(restart), int(maxit),
+                                         ras.handle if ras is not None else None, ctypes.byref(st),
+                                         stream or sf), "cpm_part_solve")
     return SolveStats(st.iterations, bool(st.converged), st.cycles, bool(st.breakdown), st.resid_est,
                       st.resid_true, st.bnorm, st.seconds)
+
+
+# ---------------------------------------------------------------- distributed RAS
+class _RasInfo(ctypes.Structure):
+    _fields_ = [("n_sub", ctypes.c_int32), ("sub0", ctypes.c_int32), ("n_sub_local", ctypes.c_int32),
+                ("rank", ctypes.c_int32), ("nranks", ctypes.c_int32), ("n_members", ctypes.c_int64),
+                ("n_owned", ctypes.c_int64), ("n_halo", ctypes.c_int64), ("n_send", ctypes.c_int64)]
+
+
+def cpm_ras_get_info(ras) -> dict:
+    inf = _RasInfo()
+    _check(load_library().cpm_ras_get_info(ras.handle, ctypes.byref(inf)), "cpm_ras_get_info")
+    return {f: getattr(inf, f) for f, _ in _RasInfo._fields_}
+
+
+def cpm_part_ras_setup(part: Part, n_sub: int, overlap: int, k_inner: int, c: float, stream=None) -> Ras:
+    out = _vp()
+    _check(load_library().cpm_part_ras_setup(part.handle, int(n_sub), int(overlap), int(k_inner), float(c),
+                                             stream, ctypes.byref(out)), "cpm_part_ras_setup")
+    return Ras(out, part.band)
+
+
+def cpm_ras_halo_nodes(ras) -> np.ndarray:
+    n = cpm_ras_get_info(ras)["n_halo"]
+    out = np.empty(n, dtype=np.int64)
+    _check(load_library().cpm_ras_halo_nodes(ras.handle, out.ctypes.data if n else None), "cpm_ras_halo_nodes")
+    return out
+
+
+def cpm_ras_set_send(ras, send_global: np.ndarray, counts: np.ndarray):
+    sg = np.ascontiguousarray(send_global, dtype=np.int64)
+    ct = np.ascontiguousarray(counts, dtype=np.int64)
+    if sg.size != int(ct.sum()):
+        raise CpmError("cpm_ras_set_send: counts must sum to len(send_global)")
+    _check(load_library().cpm_ras_set_send(ras.handle, sg.ctypes.data if sg.size else None, ct.ctypes.data),
+           "cpm_ras_set_send")
+
+
+def cpm_part_ras_apply_local(ras, r_owned, r_halo, z_owned, stream=None):
+    inf = cpm_ras_get_info(ras)
+    pr, sr = _ptr_stream(r_owned, inf["n_owned"], False)
+    ph = None
+    if inf["n_halo"]:
+        ph, _ = _ptr_stream(r_halo, inf["n_halo"], False)
+    pz, _ = _ptr_stream(z_owned, inf["n_owned"], True)
+    _check(load_library().cpm_part_ras_apply_local(ras.handle, pr, ph, pz, stream or sr),
+           "cpm_part_ras_apply_local")
+    return z_owned
+
+
+def cpm_part_ras_apply(ras, comm: Comm, r_owned, z_owned, stream=None):
+    inf = cpm_ras_get_info(ras)
+    pr, sr = _ptr_stream(r_owned, inf["n_owned"], False)
+    pz, _ = _ptr_stream(z_owned, inf["n_owned"], True)
+    _check(load_library().cpm_part_ras_apply(ras.handle, comm.handle if comm else None, pr, pz, stream or sr),
+           "cpm_part_ras_apply")
+    return z_owned

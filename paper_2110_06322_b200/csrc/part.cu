@@ -29,6 +29,7 @@
 #include "internal.cuh"
 #include "krylov.cuh"
 #include "part.cuh"
+#include "ras.cuh"
 #include "vecops.cuh"
 
 namespace cpm {
@@ -374,26 +375,38 @@ int part_set_send(cpm_part* P, const int64_t* send_global, const int64_t* counts
   return CPM_OK;
 }
 
-// Halo exchange of the owned vector x into P->hbuf (NCCL grouped send/recv).
-int part_exchange(const cpm_part* P, const cpm_comm* comm, const double* x, cudaStream_t s) {
-  if (P->nranks == 1) return CPM_OK;
-  if (!comm) return fail(CPM_ERR_ARG, "partitioned apply needs a communicator");
-  if (P->nSend > 0) {
-    k_gather_idx<<<g1(P->nSend), 256, 0, s>>>(P->nSend, P->sendidx, x, P->sendbuf);
+// Point-to-point exchange: gather x[sendidx] into sendbuf, then one NCCL group of
+// send/recv per peer (peer q's slices at sendOff[q] / recvOff[q]) into recvbuf.
+int halo_exchange(const cpm_comm* comm, int rank, int nranks, const double* x, int64_t nSend,
+                  const int64_t* sendidx, double* sendbuf, const std::vector<int64_t>& sendCount,
+                  const std::vector<int64_t>& sendOff, double* recvbuf,
+                  const std::vector<int64_t>& recvCount, const std::vector<int64_t>& recvOff,
+                  cudaStream_t s) {
+  if (nranks == 1) return CPM_OK;
+  if (!comm) return fail(CPM_ERR_ARG, "partitioned operation needs a communicator");
+  if ((int)sendCount.size() != nranks) return fail(CPM_ERR_ARG, "halo exchange: send plan not set");
+  if (nSend > 0) {
+    k_gather_idx<<<g1(nSend), 256, 0, s>>>(nSend, sendidx, x, sendbuf);
     count_launch();
   }
   CPM_TRY(nccl_check(g_nccl.GroupStart(), "ncclGroupStart"));
-  for (int q = 0; q < P->nranks; ++q) {
-    if (q == P->rank) continue;
-    if (P->sendCount[q] > 0)
-      CPM_TRY(nccl_check(g_nccl.Send(P->sendbuf + P->sendOff[q], P->sendCount[q], ncclDouble, q,
+  for (int q = 0; q < nranks; ++q) {
+    if (q == rank) continue;
+    if (sendCount[q] > 0)
+      CPM_TRY(nccl_check(g_nccl.Send(sendbuf + sendOff[q], sendCount[q], ncclDouble, q,
                                      (ncclComm_t)comm->nccl, s), "ncclSend"));
-    if (P->recvCount[q] > 0)
-      CPM_TRY(nccl_check(g_nccl.Recv(P->hbuf + P->recvOff[q], P->recvCount[q], ncclDouble, q,
+    if (recvCount[q] > 0)
+      CPM_TRY(nccl_check(g_nccl.Recv(recvbuf + recvOff[q], recvCount[q], ncclDouble, q,
                                      (ncclComm_t)comm->nccl, s), "ncclRecv"));
   }
   CPM_TRY(nccl_check(g_nccl.GroupEnd(), "ncclGroupEnd"));
   return CPM_OK;
+}
+
+// Halo exchange of the owned vector x into P->hbuf.
+int part_exchange(const cpm_part* P, const cpm_comm* comm, const double* x, cudaStream_t s) {
+  return halo_exchange(comm, P->rank, P->nranks, x, P->nSend, P->sendidx, P->sendbuf, P->sendCount,
+                       P->sendOff, P->hbuf, P->recvCount, P->recvOff, s);
 }
 
 }  // namespace cpm
@@ -487,10 +500,21 @@ int cpm_part_apply(const cpm_part* p, const cpm_comm* comm, double c, const doub
 }
 
 int cpm_part_solve(const cpm_part* p, const cpm_comm* comm, double c, const double* f_owned,
-                   double* u_owned, double rtol, int restart, int maxit, cpm_solve_stats* stats,
-                   void* stream) {
+                   double* u_owned, double rtol, int restart, int maxit, const cpm_ras* ras,
+                   cpm_solve_stats* stats, void* stream) {
   if (!p || !f_owned || !u_owned) return fail(CPM_ERR_ARG, "cpm_part_solve: null argument");
   if (p->nranks > 1 && !comm) return fail(CPM_ERR_ARG, "cpm_part_solve: needs a communicator");
+  PrecOp M;
+  if (ras) {
+    cpm_ras_info ri;
+    CPM_TRY(cpm_ras_get_info(ras, &ri));
+    if (ras->band != p->band || ri.rank != p->rank || ri.nranks != p->nranks)
+      return fail(CPM_ERR_ARG, "cpm_part_solve: preconditioner built for another partition");
+    M.apply = [ras, comm](const double* r, double* z, cudaStream_t st) {
+      CPM_TRY(ras_exchange(ras, comm, r, st));
+      return ras_apply_device(ras, r, z, st);
+    };
+  }
   LinOp A;
   A.apply = [p, comm, c](const double* x, double* y, const double* scale, cudaStream_t st) {
     CPM_TRY(part_exchange(p, comm, x, st));
@@ -498,7 +522,7 @@ int cpm_part_solve(const cpm_part* p, const cpm_comm* comm, double c, const doub
   };
   A.allreduce = [comm](double* buf, size_t n, cudaStream_t st) { return comm_allreduce_sum(comm, buf, n, st); };
   cpm_solve_stats local;
-  return gmres_device(A, nullptr, f_owned, u_owned, p->nOwned, rtol, restart, maxit, *p->ws,
+  return gmres_device(A, ras ? &M : nullptr, f_owned, u_owned, p->nOwned, rtol, restart, maxit, *p->ws,
                       stats ? stats : &local, (cudaStream_t)stream);
 }
 

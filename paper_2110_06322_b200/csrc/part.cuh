@@ -27,4 +27,10 @@ struct cpm_part {
 
 namespace cpm {
 int comm_allreduce_sum(const cpm_comm* comm, double* buf, size_t n, cudaStream_t s);
+int part_exchange(const cpm_part* P, const cpm_comm* comm, const double* x, cudaStream_t s);
+int halo_exchange(const cpm_comm* comm, int rank, int nranks, const double* x, int64_t nSend,
+                  const int64_t* sendidx, double* sendbuf, const std::vector<int64_t>& sendCount,
+                  const std::vector<int64_t>& sendOff, double* recvbuf,
+                  const std::vector<int64_t>& recvCount, const std::vector<int64_t>& recvOff,
+                  cudaStream_t s);
 }

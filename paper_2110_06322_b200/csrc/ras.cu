@@ -26,6 +26,7 @@
 
 #include "geom.cuh"
 #include "krylov.cuh"
+#include "part.cuh"
 #include "ras.cuh"
 #include "vecops.cuh"
 
@@ -235,10 +236,15 @@ __global__ void k_set_ranges(int n, TileHdr* sub, const int64_t* rowbase, const 
 }
 
 // ---------------------------------------------------------------- apply kernels
-__global__ void k_gather(int64_t n, const int64_t* gidx, const double* r, double* x) {
+// x_i = (R_j r) for every member i of the concatenated subdomains: gidx < nown
+// indexes the owned vector, larger values the received halo (distributed RAS).
+__global__ void k_gather(int64_t n, const int64_t* gidx, const double* r, const double* rh,
+                         int64_t nown, double* x) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x)
-    x[i] = r[gidx[i]];
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t g = gidx[i];
+    x[i] = g < nown ? r[g] : rh[g - nown];
+  }
 }
 
 // one thread per segment
@@ -356,8 +362,16 @@ struct RasImpl {
   InnerState* st = nullptr;
   unsigned* counters = nullptr;
   int gps = 1;
+  // distributed RAS (a rank's subdomains of a partitioned band)
+  int rank = 0, nranks = 1, sub0 = 0, nsubGlobal = 0;
+  int64_t ownLo = 0, nOwned = 0, nHalo = 0, nSend = 0;
+  std::vector<int64_t> halo_h;                       // received global indices (sorted)
+  double* hbuf = nullptr;                            // received values
+  int64_t* sendidx = nullptr;                        // owned local indices to send
+  double* sendbuf = nullptr;
+  std::vector<int64_t> sendCount, sendOff, recvCount, recvOff;
   ~RasImpl() {
-    void* ps[] = {off, gidx, lo, hi, xoff, V, W, partial, st, counters};
+    void* ps[] = {off, gidx, lo, hi, xoff, V, W, partial, st, counters, hbuf, sendidx, sendbuf};
     for (void* p : ps)
       if (p) cudaFree(p);
     void* mp[] = {mb.tiles, mb.runs, mb.vb, mb.acell};
@@ -366,8 +380,11 @@ struct RasImpl {
   }
 };
 
+// sub0, nsl: this rank's subdomains [sub0, sub0 + nsl) of S; own_lo, nown: its owned
+// band-order range (the whole band on one GPU); nranks: for the halo owners.
 int ras_setup_device(const cpm_band* B, int S, int overlap, int k, double c, cudaStream_t s,
-                     cpm_ras** out) {
+                     cpm_ras** out, int sub0, int nsl, int64_t own_lo, int64_t nown, int rank,
+                     int nranks) {
   if (!B || !out) return fail(CPM_ERR_ARG, "cpm_ras_setup: null argument");
   *out = nullptr;
   if (S < 1 || S > 64) return fail(CPM_ERR_ARG, "cpm_ras_setup: n_sub must be in [1, 64]");
@@ -376,9 +393,16 @@ int ras_setup_device(const cpm_band* B, int S, int overlap, int k, double c, cud
   if (!B->owns || B->nA < S) return fail(CPM_ERR_ARG, "cpm_ras_setup: needs a full band with n_active >= n_sub");
   const int64_t nA = B->nA;
   const int nT = B->nT;
+  if (sub0 < 0 || nsl < 1 || sub0 + nsl > S) return fail(CPM_ERR_ARG, "cpm_ras_setup: bad subdomain range");
   auto R = std::make_unique<RasImpl>();
-  R->S = S;
+  R->S = nsl;  // segments of the batched inner solves: this rank's subdomains
   R->k = k;
+  R->rank = rank;
+  R->nranks = nranks;
+  R->sub0 = sub0;
+  R->nsubGlobal = S;
+  R->ownLo = own_lo;
+  R->nOwned = nown;
 
   // neighbour table and membership bits
   DBuf nbr, bits0, bits1;
@@ -405,7 +429,7 @@ int ras_setup_device(const cpm_band* B, int S, int overlap, int k, double c, cud
   CPM_TRY(has.alloc(sizeof(int) * (size_t)(nT + 1)));
   CPM_TRY(inc.alloc(sizeof(int) * (size_t)(nT + 1)));
   CPM_TRY(incpos.alloc(sizeof(int) * (size_t)(nT + 1)));
-  std::vector<int64_t> nloc(S), ntl(S);
+  std::vector<int64_t> nloc(nsl), ntl(nsl);
   auto member_scan = [&](int sd) -> int {
     k_flag_bit<<<g1(nA + 1), 256, 0, s>>>(nA, bits, sd, flag.as<int>());
     count_launch();
@@ -418,22 +442,22 @@ int ras_setup_device(const cpm_band* B, int S, int overlap, int k, double c, cud
     CPM_CUDA(cudaGetLastError());
     return CPM_OK;
   };
-  for (int sd = 0; sd < S; ++sd) {
-    CPM_TRY(member_scan(sd));
+  for (int ls = 0; ls < nsl; ++ls) {
+    CPM_TRY(member_scan(sub0 + ls));
     int nl = 0, nt = 0;
     CPM_TRY(read1(pos.as<int>() + nA, &nl, s));
     CPM_TRY(read1(incpos.as<int>() + nT, &nt, s));
-    nloc[sd] = nl;
-    ntl[sd] = nt;
+    nloc[ls] = nl;
+    ntl[ls] = nt;
   }
-  R->off_h.assign(S + 1, 0);
-  std::vector<int64_t> toff(S + 1, 0);
-  for (int sd = 0; sd < S; ++sd) {
-    R->off_h[sd + 1] = R->off_h[sd] + nloc[sd];
-    toff[sd + 1] = toff[sd] + ntl[sd];
+  R->off_h.assign(nsl + 1, 0);
+  std::vector<int64_t> toff(nsl + 1, 0);
+  for (int ls = 0; ls < nsl; ++ls) {
+    R->off_h[ls + 1] = R->off_h[ls] + nloc[ls];
+    toff[ls + 1] = toff[ls] + ntl[ls];
   }
-  R->ntot = R->off_h[S];
-  const int nTs = (int)toff[S];
+  R->ntot = R->off_h[nsl];
+  const int nTs = (int)toff[nsl];
   if (R->ntot >= INT32_MAX) return fail(CPM_ERR_LIMIT, "cpm_ras_setup: concatenated subdomains too large");
 
   cpm_band& M = R->mb;
@@ -460,20 +484,21 @@ int ras_setup_device(const cpm_band* B, int S, int overlap, int k, double c, cud
   // phase B: per-subdomain structures
   DBuf tmap;
   CPM_TRY(tmap.alloc(sizeof(int) * (size_t)nT));
-  std::vector<DBuf> runbuf(S);
-  std::vector<int64_t> nrun(S, 0);
-  std::vector<int64_t> lo_h(S), hi_h(S), xo_h(S);
+  std::vector<DBuf> runbuf(nsl);
+  std::vector<int64_t> nrun(nsl, 0);
+  std::vector<int64_t> lo_h(nsl), hi_h(nsl), xo_h(nsl);
   DBuf dblo, dbdim;
   CPM_TRY(dblo.alloc(3 * sizeof(int)));
   CPM_TRY(dbdim.alloc(3 * sizeof(int)));
   CPM_CUDA(cudaMemcpyAsync(dblo.p, B->blo, 3 * sizeof(int), cudaMemcpyHostToDevice, s));
   CPM_CUDA(cudaMemcpyAsync(dbdim.p, B->bdim, 3 * sizeof(int), cudaMemcpyHostToDevice, s));
-  for (int sd = 0; sd < S; ++sd) {
+  for (int ls = 0; ls < nsl; ++ls) {
+    const int sd = sub0 + ls;  // global subdomain (membership bit), ls its segment here
     CPM_TRY(member_scan(sd));
-    const int64_t loff = R->off_h[sd];
-    const int to = (int)toff[sd], nt = (int)ntl[sd];
+    const int64_t loff = R->off_h[ls];
+    const int to = (int)toff[ls], nt = (int)ntl[ls];
     k_subtiles<<<(nT + 255) / 256, 256, 0, s>>>(nT, B->tiles, inc.as<int>(), incpos.as<int>(),
-                                                 pos.as<int>(), loff, to, sd, M.tiles, tmap.as<int>());
+                                                 pos.as<int>(), loff, to, ls, M.tiles, tmap.as<int>());
     count_launch();
     if (nt > 0) {
       k_subtile_nbrs<<<(nt + 255) / 256, 256, 0, s>>>(nt, M.tiles + to, tmap.as<int>());
@@ -486,9 +511,9 @@ int ras_setup_device(const cpm_band* B, int S, int overlap, int k, double c, cud
     const int64_t d0 = slab_lo(sd, nA, S), d1 = slab_lo(sd + 1, nA, S);
     int ld0 = 0;
     CPM_TRY(read1(pos.as<int>() + d0, &ld0, s));
-    lo_h[sd] = ld0;
-    hi_h[sd] = ld0 + (d1 - d0);
-    xo_h[sd] = d0;
+    lo_h[ls] = ld0;
+    hi_h[ls] = ld0 + (d1 - d0);
+    xo_h[ls] = d0 - own_lo;  // the disjoint slab lies in this rank's owned range
     // runs
     if (nt > 0) {
       DBuf nrows, rowbase, rowcnt, runstart;
@@ -510,52 +535,83 @@ int ras_setup_device(const cpm_band* B, int S, int overlap, int k, double c, cud
       CPM_TRY(scan(rowcnt.as<int64_t>(), runstart.as<int64_t>(), rows + 1, s));
       int64_t nr = 0;
       CPM_TRY(read1(runstart.as<int64_t>() + rows, &nr, s));
-      CPM_TRY(runbuf[sd].alloc(sizeof(uint64_t) * (size_t)nr));
+      CPM_TRY(runbuf[ls].alloc(sizeof(uint64_t) * (size_t)nr));
       k_sub_runs<true><<<nt, 128, 0, s>>>(M.tiles + to, B->tiles, B->amask, B->bmap, dblo.as<int>(),
                                           dbdim.as<int>(), bits, sd, pos.as<int>(), loff,
                                           rowbase.as<int64_t>(), rowcnt.as<int64_t>(),
-                                          runstart.as<int64_t>(), runbuf[sd].as<uint64_t>());
+                                          runstart.as<int64_t>(), runbuf[ls].as<uint64_t>());
       count_launch();
       int64_t roff = 0;
-      for (int q = 0; q < sd; ++q) roff += nrun[q];
+      for (int q = 0; q < ls; ++q) roff += nrun[q];
       k_set_ranges<<<(nt + 255) / 256, 256, 0, s>>>(nt, M.tiles + to, rowbase.as<int64_t>(),
                                                      runstart.as<int64_t>(), roff);
       count_launch();
-      nrun[sd] = nr;
+      nrun[ls] = nr;
       CPM_CUDA(cudaStreamSynchronize(s));
     }
     CPM_CUDA(cudaGetLastError());
   }
   int64_t totRuns = 0;
-  for (int sd = 0; sd < S; ++sd) totRuns += nrun[sd];
+  for (int ls = 0; ls < nsl; ++ls) totRuns += nrun[ls];
   if (totRuns >= (int64_t)INT32_MAX) return fail(CPM_ERR_LIMIT, "cpm_ras_setup: too many runs");
   CPM_CUDA(cudaMalloc(&M.runs, sizeof(uint64_t) * std::max<int64_t>(totRuns, 1)));
-  for (int sd = 0, ro = 0; sd < S; ro += (int)nrun[sd], ++sd)
-    if (nrun[sd] > 0)
-      CPM_CUDA(cudaMemcpyAsync(M.runs + ro, runbuf[sd].p, sizeof(uint64_t) * nrun[sd],
+  for (int ls = 0, ro = 0; ls < nsl; ro += (int)nrun[ls], ++ls)
+    if (nrun[ls] > 0)
+      CPM_CUDA(cudaMemcpyAsync(M.runs + ro, runbuf[ls].p, sizeof(uint64_t) * nrun[ls],
                                cudaMemcpyDeviceToDevice, s));
   M.nRuns = totRuns;
 
+  // members outside the owned range come from other ranks (the RAS halo): gidx
+  // becomes an index into [owned | halo]
+  if (own_lo != 0 || nown != nA) {
+    std::vector<int64_t> g(R->ntot);
+    if (R->ntot > 0)
+      CPM_CUDA(cudaMemcpy(g.data(), R->gidx, sizeof(int64_t) * R->ntot, cudaMemcpyDeviceToHost));
+    std::vector<int64_t>& H = R->halo_h;
+    for (int64_t v : g)
+      if (v < own_lo || v >= own_lo + nown) H.push_back(v);
+    std::sort(H.begin(), H.end());
+    H.erase(std::unique(H.begin(), H.end()), H.end());
+    for (int64_t& v : g)
+      v = (v >= own_lo && v < own_lo + nown) ? v - own_lo
+                                             : nown + (std::lower_bound(H.begin(), H.end(), v) - H.begin());
+    if (R->ntot > 0)
+      CPM_CUDA(cudaMemcpy(R->gidx, g.data(), sizeof(int64_t) * R->ntot, cudaMemcpyHostToDevice));
+    R->nHalo = (int64_t)H.size();
+    CPM_CUDA(cudaMalloc(&R->hbuf, sizeof(double) * std::max<int64_t>(R->nHalo, 1)));
+    // receive plan: the halo is sorted, hence grouped by owner (slab bounds, reading R8)
+    R->recvCount.assign(nranks, 0);
+    R->recvOff.assign(nranks + 1, 0);
+    for (int64_t v : H) {
+      int q = (int)((v * nranks) / nA);
+      while (q + 1 < nranks && v >= slab_lo(q + 1, nA, nranks)) ++q;
+      while (q > 0 && v < slab_lo(q, nA, nranks)) --q;
+      R->recvCount[q]++;
+    }
+    for (int q = 0; q < nranks; ++q) R->recvOff[q + 1] = R->recvOff[q] + R->recvCount[q];
+    if (R->recvCount[rank] != 0) return fail(CPM_ERR_GEOM, "cpm_part_ras_setup: halo contains owned nodes");
+  }
+
   // segment tables and inner workspace
-  CPM_CUDA(cudaMalloc(&R->off, sizeof(int64_t) * (S + 1)));
-  CPM_CUDA(cudaMalloc(&R->lo, sizeof(int64_t) * S));
-  CPM_CUDA(cudaMalloc(&R->hi, sizeof(int64_t) * S));
-  CPM_CUDA(cudaMalloc(&R->xoff, sizeof(int64_t) * S));
-  CPM_CUDA(cudaMemcpyAsync(R->off, R->off_h.data(), sizeof(int64_t) * (S + 1), cudaMemcpyHostToDevice, s));
-  CPM_CUDA(cudaMemcpyAsync(R->lo, lo_h.data(), sizeof(int64_t) * S, cudaMemcpyHostToDevice, s));
-  CPM_CUDA(cudaMemcpyAsync(R->hi, hi_h.data(), sizeof(int64_t) * S, cudaMemcpyHostToDevice, s));
-  CPM_CUDA(cudaMemcpyAsync(R->xoff, xo_h.data(), sizeof(int64_t) * S, cudaMemcpyHostToDevice, s));
+  CPM_CUDA(cudaMalloc(&R->off, sizeof(int64_t) * (nsl + 1)));
+  CPM_CUDA(cudaMalloc(&R->lo, sizeof(int64_t) * nsl));
+  CPM_CUDA(cudaMalloc(&R->hi, sizeof(int64_t) * nsl));
+  CPM_CUDA(cudaMalloc(&R->xoff, sizeof(int64_t) * nsl));
+  CPM_CUDA(cudaMemcpyAsync(R->off, R->off_h.data(), sizeof(int64_t) * (nsl + 1), cudaMemcpyHostToDevice, s));
+  CPM_CUDA(cudaMemcpyAsync(R->lo, lo_h.data(), sizeof(int64_t) * nsl, cudaMemcpyHostToDevice, s));
+  CPM_CUDA(cudaMemcpyAsync(R->hi, hi_h.data(), sizeof(int64_t) * nsl, cudaMemcpyHostToDevice, s));
+  CPM_CUDA(cudaMemcpyAsync(R->xoff, xo_h.data(), sizeof(int64_t) * nsl, cudaMemcpyHostToDevice, s));
   R->ldv = (R->ntot + 63) / 64 * 64;
   CPM_CUDA(cudaMalloc(&R->V, sizeof(double) * (size_t)R->ldv * (k + 1)));
   CPM_CUDA(cudaMalloc(&R->W, sizeof(double) * (size_t)R->ldv));
   int64_t maxn = 0;
-  for (int sd = 0; sd < S; ++sd) maxn = std::max(maxn, nloc[sd]);
-  R->gps = (int)std::max<int64_t>(1, std::min<int64_t>((maxn + 255) / 256, std::max(1, kMaxBlocks / S / 2)));
-  CPM_CUDA(cudaMalloc(&R->partial, sizeof(double) * (size_t)S * R->gps * (kMaxRestart + 8)));
-  CPM_CUDA(cudaMalloc(&R->st, sizeof(InnerState) * S));
-  CPM_CUDA(cudaMemsetAsync(R->st, 0, sizeof(InnerState) * S, s));
-  CPM_CUDA(cudaMalloc(&R->counters, sizeof(unsigned) * S * 4));
-  CPM_CUDA(cudaMemsetAsync(R->counters, 0, sizeof(unsigned) * S * 4, s));
+  for (int ls = 0; ls < nsl; ++ls) maxn = std::max(maxn, nloc[ls]);
+  R->gps = (int)std::max<int64_t>(1, std::min<int64_t>((maxn + 255) / 256, std::max(1, kMaxBlocks / nsl / 2)));
+  CPM_CUDA(cudaMalloc(&R->partial, sizeof(double) * (size_t)nsl * R->gps * (kMaxRestart + 8)));
+  CPM_CUDA(cudaMalloc(&R->st, sizeof(InnerState) * nsl));
+  CPM_CUDA(cudaMemsetAsync(R->st, 0, sizeof(InnerState) * nsl, s));
+  CPM_CUDA(cudaMalloc(&R->counters, sizeof(unsigned) * nsl * 4));
+  CPM_CUDA(cudaMemsetAsync(R->counters, 0, sizeof(unsigned) * nsl * 4, s));
   CPM_CUDA(cudaStreamSynchronize(s));
 
   cpm_ras* ras = new cpm_ras();
@@ -569,8 +625,10 @@ int ras_setup_device(const cpm_band* B, int S, int overlap, int k, double c, cud
   return CPM_OK;
 }
 
-int ras_apply_device(const cpm_ras* ras, const double* r, double* z, cudaStream_t s) {
+int ras_apply_device(const cpm_ras* ras, const double* r, double* z, cudaStream_t s,
+                     const double* r_halo) {
   RasImpl* R = (RasImpl*)ras->impl;
+  if (!r_halo) r_halo = R->hbuf;
   const int S = R->S, k = R->k;
   const vec::Seg Sg{R->off, S, R->gps};
   const int grid = S * R->gps;
@@ -586,7 +644,7 @@ int ras_apply_device(const cpm_ras* ras, const double* r, double* z, cudaStream_
   const int o_y = (int)(offsetof(InnerState, y) / sizeof(double));
   {
     ProfScope ps(K_OTHER, s);
-    k_gather<<<g1(R->ntot), 256, 0, s>>>(R->ntot, R->gidx, r, R->V);
+    k_gather<<<g1(R->ntot), 256, 0, s>>>(R->ntot, R->gidx, r, r_halo, R->nOwned, R->V);
     count_launch();
     vec::k_sub_nrm2<<<grid, VB, 0, s>>>(Sg, R->V, nullptr, nullptr, R->partial, base + o_beta2, lds,
                                         R->counters);
@@ -634,17 +692,110 @@ int ras_apply_device(const cpm_ras* ras, const double* r, double* z, cudaStream_
   return CPM_OK;
 }
 
+int ras_exchange(const cpm_ras* ras, const cpm_comm* comm, const double* r_owned, cudaStream_t s) {
+  const RasImpl* R = (const RasImpl*)ras->impl;
+  if (R->nranks == 1) return CPM_OK;
+  return halo_exchange(comm, R->rank, R->nranks, r_owned, R->nSend, R->sendidx, R->sendbuf,
+                       R->sendCount, R->sendOff, R->hbuf, R->recvCount, R->recvOff, s);
+}
+
 }  // namespace cpm
 
 using namespace cpm;
 extern "C" {
 int cpm_ras_setup(const cpm_band* band, int n_sub, int overlap, int k_inner, double c, void* stream,
                   cpm_ras** out) {
-  return ras_setup_device(band, n_sub, overlap, k_inner, c, (cudaStream_t)stream, out);
+  if (!band) return fail(CPM_ERR_ARG, "cpm_ras_setup: null argument");
+  return ras_setup_device(band, n_sub, overlap, k_inner, c, (cudaStream_t)stream, out, 0, n_sub, 0,
+                          band->nA, 0, 1);
+}
+
+int cpm_part_ras_setup(const cpm_part* part, int n_sub, int overlap, int k_inner, double c,
+                       void* stream, cpm_ras** out) {
+  if (!part || !out) return fail(CPM_ERR_ARG, "cpm_part_ras_setup: null argument");
+  const int R = part->nranks;
+  if (n_sub < R || n_sub % R != 0)
+    return fail(CPM_ERR_ARG, "cpm_part_ras_setup: n_sub must be a multiple of the number of ranks "
+                             "(PAPER.md:213)");
+  const int per = n_sub / R;
+  return ras_setup_device(part->band, n_sub, overlap, k_inner, c, (cudaStream_t)stream, out,
+                          part->rank * per, per, part->lo, part->nOwned, part->rank, R);
+}
+
+int cpm_ras_get_info(const cpm_ras* ras, cpm_ras_info* info) {
+  if (!ras || !info) return fail(CPM_ERR_ARG, "cpm_ras_get_info: null argument");
+  const RasImpl* R = (const RasImpl*)ras->impl;
+  memset(info, 0, sizeof(*info));
+  info->n_sub = R->nsubGlobal;
+  info->sub0 = R->sub0;
+  info->n_sub_local = R->S;
+  info->rank = R->rank;
+  info->nranks = R->nranks;
+  info->n_members = R->ntot;
+  info->n_owned = R->nOwned;
+  info->n_halo = R->nHalo;
+  info->n_send = R->nSend;
+  return CPM_OK;
+}
+
+int cpm_ras_halo_nodes(const cpm_ras* ras, int64_t* halo_host) {
+  if (!ras) return fail(CPM_ERR_ARG, "cpm_ras_halo_nodes: null argument");
+  const RasImpl* R = (const RasImpl*)ras->impl;
+  if (R->nHalo > 0 && !halo_host) return fail(CPM_ERR_ARG, "cpm_ras_halo_nodes: null output");
+  if (R->nHalo > 0) memcpy(halo_host, R->halo_h.data(), sizeof(int64_t) * R->nHalo);
+  return CPM_OK;
+}
+
+int cpm_ras_set_send(cpm_ras* ras, const int64_t* send_global, const int64_t* counts) {
+  if (!ras || !counts) return fail(CPM_ERR_ARG, "cpm_ras_set_send: null argument");
+  RasImpl* R = (RasImpl*)ras->impl;
+  const int nr = R->nranks;
+  R->sendCount.assign(counts, counts + nr);
+  R->sendOff.assign(nr + 1, 0);
+  for (int q = 0; q < nr; ++q) {
+    if (counts[q] < 0) return fail(CPM_ERR_ARG, "cpm_ras_set_send: negative count");
+    R->sendOff[q + 1] = R->sendOff[q] + counts[q];
+  }
+  const int64_t n = R->sendOff[nr];
+  if (n > 0 && !send_global) return fail(CPM_ERR_ARG, "cpm_ras_set_send: null index list");
+  std::vector<int64_t> loc(n);
+  for (int64_t i = 0; i < n; ++i) {
+    const int64_t a = send_global[i];
+    if (a < R->ownLo || a >= R->ownLo + R->nOwned)
+      return fail(CPM_ERR_ARG, "cpm_ras_set_send: requested node not owned");
+    loc[i] = a - R->ownLo;
+  }
+  if (R->sendidx) cudaFree(R->sendidx);
+  if (R->sendbuf) cudaFree(R->sendbuf);
+  R->sendidx = nullptr;
+  R->sendbuf = nullptr;
+  CPM_CUDA(cudaMalloc(&R->sendidx, sizeof(int64_t) * std::max<int64_t>(n, 1)));
+  CPM_CUDA(cudaMalloc(&R->sendbuf, sizeof(double) * std::max<int64_t>(n, 1)));
+  if (n > 0) CPM_CUDA(cudaMemcpy(R->sendidx, loc.data(), sizeof(int64_t) * n, cudaMemcpyHostToDevice));
+  R->nSend = n;
+  return CPM_OK;
+}
+
+int cpm_part_ras_apply_local(const cpm_ras* ras, const double* r_owned, const double* r_halo,
+                             double* z_owned, void* stream) {
+  if (!ras || !r_owned || !z_owned) return fail(CPM_ERR_ARG, "cpm_part_ras_apply_local: null argument");
+  const RasImpl* R = (const RasImpl*)ras->impl;
+  if (R->nHalo > 0 && !r_halo) return fail(CPM_ERR_ARG, "cpm_part_ras_apply_local: null halo");
+  return ras_apply_device(ras, r_owned, z_owned, (cudaStream_t)stream, r_halo ? r_halo : R->hbuf);
+}
+
+int cpm_part_ras_apply(const cpm_ras* ras, const cpm_comm* comm, const double* r_owned,
+                       double* z_owned, void* stream) {
+  if (!ras || !r_owned || !z_owned) return fail(CPM_ERR_ARG, "cpm_part_ras_apply: null argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  CPM_TRY(ras_exchange(ras, comm, r_owned, s));
+  return ras_apply_device(ras, r_owned, z_owned, s);
 }
 
 int cpm_ras_apply(const cpm_ras* ras, const double* r, double* z, void* stream) {
   if (!ras || !r || !z) return fail(CPM_ERR_ARG, "cpm_ras_apply: null argument");
+  if (((const RasImpl*)ras->impl)->nOwned != ras->band->nA)
+    return fail(CPM_ERR_ARG, "cpm_ras_apply: partitioned preconditioner (use cpm_part_ras_apply)");
   if ((const void*)r == (const void*)z) return fail(CPM_ERR_ARG, "cpm_ras_apply: r and z must not alias");
   cudaStream_t s = (cudaStream_t)stream;
   const int64_t n = ras->band->nA;

@@ -3,6 +3,8 @@
 #include "internal.cuh"
 #include "krylov.cuh"
 
+struct cpm_comm;
+
 struct cpm_ras {
   const cpm_band* band = nullptr;
   int nsub = 0, overlap = 0, k = 0;
@@ -23,5 +25,11 @@ struct InnerState {
   int kk, pad_;
 };
 static_assert(sizeof(InnerState) % sizeof(double) == 0, "InnerState stride");
-int ras_apply_device(const cpm_ras* r, const double* in, double* out, cudaStream_t s);
+// z = M r; r_halo: received RAS-halo values (distributed RAS; null: the internal buffer)
+int ras_apply_device(const cpm_ras* r, const double* in, double* out, cudaStream_t s,
+                     const double* r_halo = nullptr);
+int ras_setup_device(const cpm_band* B, int S, int overlap, int k, double c, cudaStream_t s,
+                     cpm_ras** out, int sub0, int nsl, int64_t own_lo, int64_t nown, int rank,
+                     int nranks);
+int ras_exchange(const cpm_ras* ras, const cpm_comm* comm, const double* r_owned, cudaStream_t s);
 }

@@ -27,6 +27,10 @@ extern "C" int cpm_solve(const cpm_band* b, double c, const double* f, double* u
   PrecOp M;
   if (ras) {
     if (ras->band != b) return fail(CPM_ERR_ARG, "cpm_solve: preconditioner built for another band");
+    cpm_ras_info ri;
+    CPM_TRY(cpm_ras_get_info(ras, &ri));
+    if (ri.n_owned != b->nA)
+      return fail(CPM_ERR_ARG, "cpm_solve: partitioned preconditioner (use cpm_part_solve)");
     M.apply = [ras](const double* r, double* z, cudaStream_t st) { return ras_apply_device(ras, r, z, st); };
   }
   const bool df = is_device_ptr(f), du = is_device_ptr(u);

@@ -103,7 +103,18 @@ class DistributedCPM:
 
         return cpm.cpm_part_apply(self.part, self.comm, c, u_owned, y_owned)
 
-    def solve(self, c, f_owned, u_owned, rtol=1e-10, restart=50, maxit=100000):
+    def setup_ras(self, n_sub, overlap, k_inner, c, group=None):
+        """This rank's RAS subdomains (n_sub a multiple of the rank count) and the
+        exchange plan of its RAS halo (the overlap reaching into other slabs)."""
         from . import cpm
 
-        return cpm.cpm_part_solve(self.part, self.comm, c, f_owned, u_owned, rtol, restart, maxit)
+        ras = cpm.cpm_part_ras_setup(self.part, n_sub, overlap, k_inner, c)
+        halo = cpm.cpm_ras_halo_nodes(ras)
+        send, counts = exchange_requests(halo, slab_bounds(self.band.n, self.nranks), group)
+        cpm.cpm_ras_set_send(ras, send, counts)
+        return ras
+
+    def solve(self, c, f_owned, u_owned, rtol=1e-10, restart=50, maxit=100000, ras=None):
+        from . import cpm
+
+        return cpm.cpm_part_solve(self.part, self.comm, c, f_owned, u_owned, rtol, restart, maxit, ras=ras)
