@@ -99,19 +99,21 @@ const bool g_force_cgs2 = [] {
   const char* v = getenv("CPM_CGS2");
   return v && *v && *v != '0';
 }();
+}  // namespace
 
 int launch_dcgs_dots(const vec::Seg& S, int k, const double* V, int64_t ldv, const double* z,
-                     double* partial, double* out, unsigned* counters, cudaStream_t st) {
+                     double* partial, int pld, double* out, int ldo, unsigned* counters,
+                     cudaStream_t st) {
   const int grid = S.nseg * S.gps;
-  const size_t sm = ((size_t)k * (256 + 4) + 256) * sizeof(double);
   if (k <= 64) {
+    const size_t sm = ((size_t)k * (256 + 4) + 256) * sizeof(double);
     static bool attr = false;
     if (!attr) {
       CPM_CUDA(cudaFuncSetAttribute(vec::k_dcgs_dots<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)(((size_t)64 * 260 + 256) * sizeof(double))));
       attr = true;
     }
-    vec::k_dcgs_dots<256><<<grid, 256, sm, st>>>(S, k, V, ldv, z, partial, 2 * kLdc + 8, out, 0, counters);
+    vec::k_dcgs_dots<256><<<grid, 256, sm, st>>>(S, k, V, ldv, z, partial, pld, out, ldo, counters);
   } else {
     static bool attr = false;
     const size_t sm2 = ((size_t)k * (128 + 4) + 128) * sizeof(double);
@@ -120,7 +122,7 @@ int launch_dcgs_dots(const vec::Seg& S, int k, const double* V, int64_t ldv, con
                                     (int)(((size_t)(kMaxRestart + 1) * 132 + 128) * sizeof(double))));
       attr = true;
     }
-    vec::k_dcgs_dots<128><<<grid, 128, sm2, st>>>(S, k, V, ldv, z, partial, 2 * kLdc + 8, out, 0, counters);
+    vec::k_dcgs_dots<128><<<grid, 128, sm2, st>>>(S, k, V, ldv, z, partial, pld, out, ldo, counters);
   }
   count_launch();
   CPM_CUDA(cudaGetLastError());
@@ -128,7 +130,7 @@ int launch_dcgs_dots(const vec::Seg& S, int k, const double* V, int64_t ldv, con
 }
 
 int launch_dcgs_update(const vec::Seg& S, int k, double* V, int64_t ldv, const double* z,
-                       const double* coef, cudaStream_t st) {
+                       const double* coef, int ldc, int64_t cstride, cudaStream_t st) {
   const int grid = S.nseg * S.gps;
   if (k <= 64) {
     const size_t sm = ((size_t)k * (256 + 4) + 2 * (size_t)k) * sizeof(double);
@@ -138,7 +140,7 @@ int launch_dcgs_update(const vec::Seg& S, int k, double* V, int64_t ldv, const d
                                     (int)(((size_t)64 * 260 + 128) * sizeof(double))));
       attr = true;
     }
-    vec::k_dcgs_update<256><<<grid, 256, sm, st>>>(S, k, V, ldv, z, coef, kLdc);
+    vec::k_dcgs_update<256><<<grid, 256, sm, st>>>(S, k, V, ldv, z, coef, ldc, cstride);
   } else {
     const size_t sm = ((size_t)k * (128 + 4) + 2 * (size_t)k) * sizeof(double);
     static bool attr = false;
@@ -147,13 +149,12 @@ int launch_dcgs_update(const vec::Seg& S, int k, double* V, int64_t ldv, const d
                                     (int)(((size_t)(kMaxRestart + 1) * 132 + 2 * (kMaxRestart + 1)) * sizeof(double))));
       attr = true;
     }
-    vec::k_dcgs_update<128><<<grid, 128, sm, st>>>(S, k, V, ldv, z, coef, kLdc);
+    vec::k_dcgs_update<128><<<grid, 128, sm, st>>>(S, k, V, ldv, z, coef, ldc, cstride);
   }
   count_launch();
   CPM_CUDA(cudaGetLastError());
   return CPM_OK;
 }
-}  // namespace
 
 namespace {
 
@@ -445,7 +446,7 @@ int gmres_device(const LinOp& A, const PrecOp* M, const double* b, double* x, in
         const int k = j + 1;
         {
           ProfScope ps(K_MDOT, s);
-          CPM_TRY(launch_dcgs_dots(S, k, ws.V, ws.ldv, ws.w, ws.partial, st->red, cnt + 1, s));
+          CPM_TRY(launch_dcgs_dots(S, k, ws.V, ws.ldv, ws.w, ws.partial, 2 * kLdc + 8, st->red, 0, cnt + 1, s));
           CPM_TRY(allreduce(st->red, 2 * k));
         }
         {
@@ -458,7 +459,7 @@ int gmres_device(const LinOp& A, const PrecOp* M, const double* b, double* x, in
         if (ws.hst->done || its >= maxit) break;
         {
           ProfScope ps(K_CGS_UPDATE, s);
-          CPM_TRY(launch_dcgs_update(S, k, ws.V, ws.ldv, ws.w, st->coef, s));
+          CPM_TRY(launch_dcgs_update(S, k, ws.V, ws.ldv, ws.w, st->coef, kLdc, 0, s));
         }
       }
     } else

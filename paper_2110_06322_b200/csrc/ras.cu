@@ -259,35 +259,100 @@ __global__ void k_inner_init(InnerState* st, int S, int k) {
   q.kk = beta > 0.0 ? k : 0;
 }
 
-__global__ void k_inner_step(InnerState* st, int S, int j) {
-  const int s = threadIdx.x;
-  if (s >= S) return;
-  InnerState& q = st[s];
-  constexpr int ld = kMaxInner + 1;
-  double* H = q.H + (size_t)j * ld;
-  for (int i = 0; i <= j; ++i) H[i] = q.h1[i] + q.h2[i];
-  const double nrm = sqrt(q.nrm2);
-  H[j + 1] = nrm;
-  for (int i = 0; i < j; ++i) {
-    const double t = q.cs[i] * H[i] + q.sn[i] * H[i + 1];
-    H[i + 1] = -q.sn[i] * H[i] + q.cs[i] * H[i + 1];
-    H[i] = t;
+// Delayed-CGS2 step j of every segment's inner GMRES (one block per segment), the
+// arithmetic of krylov.cu k_dcgs_step without a convergence test: finalise column
+// j-1 ([cpend + b; rho], Givens), then the coefficients of the update pass.
+constexpr int kInnerStepThreads = 64;
+__global__ void __launch_bounds__(kInnerStepThreads) k_inner_dcgs_step(InnerState* st, int j) {
+  InnerState& q = st[blockIdx.x];
+  constexpr int ld = kMaxInner + 1, ldc = kMaxInner + 2;
+  const int k = j + 1, tid = threadIdx.x;
+  const double* b = q.red;
+  const double* d = q.red + k;
+  __shared__ double sbb[kInnerStepThreads / 32], sbd[kInnerStepThreads / 32];
+  __shared__ int sstop;
+  double pbb = 0.0, pbd = 0.0;
+  for (int i = tid; i < j; i += kInnerStepThreads) {
+    pbb += b[i] * b[i];
+    pbd += b[i] * d[i];
   }
-  const double den = hypot(H[j], H[j + 1]);
-  if (den == 0.0) {
-    q.cs[j] = 1.0;
-    q.sn[j] = 0.0;
-  } else {
-    q.cs[j] = H[j] / den;
-    q.sn[j] = H[j + 1] / den;
+  pbb = vec::warp_sum(pbb);
+  pbd = vec::warp_sum(pbd);
+  if ((tid & 31) == 0) {
+    sbb[tid >> 5] = pbb;
+    sbd[tid >> 5] = pbd;
   }
-  const bool brk = H[j + 1] == 0.0;
-  H[j] = q.cs[j] * H[j] + q.sn[j] * H[j + 1];
-  H[j + 1] = 0.0;
-  q.g[j + 1] = -q.sn[j] * q.g[j];
-  q.g[j] = q.cs[j] * q.g[j];
-  q.sc[j + 1] = nrm > 0.0 ? 1.0 / nrm : 0.0;
-  if (brk && q.kk > j + 1) q.kk = j + 1;  // happy breakdown: solution in the first j+1 steps
+  __syncthreads();
+  double bb = 0.0, bd = 0.0;
+  for (int w = 0; w < kInnerStepThreads / 32; ++w) {
+    bb += sbb[w];
+    bd += sbd[w];
+  }
+  const double alpha = q.red[j], gamma = q.red[k + j];
+  const double rho2 = alpha - bb;
+  const bool brk = !(rho2 > 1e-28 * alpha);
+  const double rho = brk ? 1.0 : sqrt(rho2);  // broken: the segment stops at kk = j
+  if (j >= 1)
+    for (int i = tid; i < j; i += kInnerStepThreads) q.Hr[(size_t)(j - 1) * ld + i] = q.cpend[i] + b[i];
+  __syncthreads();
+  if (tid == 0) {
+    sstop = 0;
+    if (j == 0) {
+      q.g[0] *= brk ? 0.0 : rho;  // u_0 = r_j / beta: r_j = (beta rho) q_0
+      if (brk) q.kk = 0;
+    } else if (q.kk >= j) {
+      double* Hr = q.Hr + (size_t)(j - 1) * ld;
+      double* H = q.H + (size_t)(j - 1) * ld;
+      Hr[j] = brk ? 0.0 : rho;
+      for (int i = 0; i <= j; ++i) H[i] = Hr[i];
+      const int c = j - 1;
+      for (int i = 0; i < c; ++i) {
+        const double t = q.cs[i] * H[i] + q.sn[i] * H[i + 1];
+        H[i + 1] = -q.sn[i] * H[i] + q.cs[i] * H[i + 1];
+        H[i] = t;
+      }
+      const double den = hypot(H[c], H[c + 1]);
+      if (den == 0.0) {
+        q.cs[c] = 1.0;
+        q.sn[c] = 0.0;
+      } else {
+        q.cs[c] = H[c] / den;
+        q.sn[c] = H[c + 1] / den;
+      }
+      H[c] = q.cs[c] * H[c] + q.sn[c] * H[c + 1];
+      H[c + 1] = 0.0;
+      q.g[c + 1] = -q.sn[c] * q.g[c];
+      q.g[c] = q.cs[c] * q.g[c];
+      if (brk && q.kk > j) q.kk = j;  // happy breakdown: solution in the first j columns
+    }
+    if (brk) sstop = 1;
+  }
+  __syncthreads();
+  double* cb = q.coef;
+  double* ce = q.coef + ldc;
+  if (sstop) {  // harmless coefficients for the (unused) rest of this segment
+    for (int i = tid; i < j; i += kInnerStepThreads) cb[i] = ce[i] = 0.0;
+    if (tid == 0) {
+      q.coef[2 * ldc] = 1.0;
+      q.coef[2 * ldc + 1] = 0.0;
+    }
+    return;
+  }
+  const double mu = (gamma - bd) / rho2;
+  for (int l = tid; l <= j; l += kInnerStepThreads) {
+    double gl = 0.0;  // (Hr b)_l
+    for (int i = (l > 0 ? l - 1 : 0); i < j; ++i) gl += q.Hr[(size_t)i * ld + l] * b[i];
+    const double ql = l < j ? d[l] : rho * mu;
+    q.cpend[l] = (ql - gl) / rho;
+  }
+  for (int i = tid; i < j; i += kInnerStepThreads) {
+    cb[i] = b[i];
+    ce[i] = d[i] - mu * b[i];
+  }
+  if (tid == 0) {
+    q.coef[2 * ldc] = rho;
+    q.coef[2 * ldc + 1] = mu;
+  }
 }
 
 __global__ void k_inner_lsq(InnerState* st) {
@@ -607,7 +672,7 @@ int ras_setup_device(const cpm_band* B, int S, int overlap, int k, double c, cud
   int64_t maxn = 0;
   for (int ls = 0; ls < nsl; ++ls) maxn = std::max(maxn, nloc[ls]);
   R->gps = (int)std::max<int64_t>(1, std::min<int64_t>((maxn + 255) / 256, std::max(1, kMaxBlocks / nsl / 2)));
-  CPM_CUDA(cudaMalloc(&R->partial, sizeof(double) * (size_t)nsl * R->gps * (kMaxRestart + 8)));
+  CPM_CUDA(cudaMalloc(&R->partial, sizeof(double) * (size_t)nsl * R->gps * (2 * (kMaxInner + 2) + 8)));
   CPM_CUDA(cudaMalloc(&R->st, sizeof(InnerState) * nsl));
   CPM_CUDA(cudaMemsetAsync(R->st, 0, sizeof(InnerState) * nsl, s));
   CPM_CUDA(cudaMalloc(&R->counters, sizeof(unsigned) * nsl * 4));
@@ -637,10 +702,7 @@ int ras_apply_device(const cpm_ras* ras, const double* r, double* z, cudaStream_
   double* base = (double*)st;
   // member offsets inside InnerState, in doubles
   const int o_beta2 = (int)(offsetof(InnerState, beta2) / sizeof(double));
-  const int o_nrm2 = (int)(offsetof(InnerState, nrm2) / sizeof(double));
   const int o_sc = (int)(offsetof(InnerState, sc) / sizeof(double));
-  const int o_h1 = (int)(offsetof(InnerState, h1) / sizeof(double));
-  const int o_h2 = (int)(offsetof(InnerState, h2) / sizeof(double));
   const int o_y = (int)(offsetof(InnerState, y) / sizeof(double));
   {
     ProfScope ps(K_OTHER, s);
@@ -652,30 +714,30 @@ int ras_apply_device(const cpm_ras* ras, const double* r, double* z, cudaStream_
     k_inner_init<<<1, 64, 0, s>>>(st, S, k);
     count_launch();
   }
-  for (int j = 0; j < k; ++j) {
-    const double* Vj = R->V + (size_t)j * R->ldv;
-    CPM_TRY(apply_device(&R->mb, ras->c, Vj, R->W, base + o_sc + j, lds, s));
-    const int kk = j + 1;
+  const int o_red = (int)(offsetof(InnerState, red) / sizeof(double));
+  const int o_coef = (int)(offsetof(InnerState, coef) / sizeof(double));
+  {  // V_0 = R_j r / beta_j: the first lagged vector of every segment
+    ProfScope ps(K_AXPY, s);
+    vec::k_scale<<<grid, VB, 0, s>>>(Sg, R->V, base + o_sc, lds, 0, R->V);
+    count_launch();
+  }
+  // delayed CGS2 (krylov.cu): per inner step one apply, one reduction pass, one
+  // update pass; step k only finalises the last Hessenberg column
+  for (int j = 0; j <= k; ++j) {
+    if (j < k) CPM_TRY(apply_device(&R->mb, ras->c, R->V + (size_t)j * R->ldv, R->W, nullptr, 0, s));
     {
       ProfScope ps(K_MDOT, s);
-      CPM_TRY(launch_mdot(Sg, kk, R->V, R->ldv, R->W, base + o_sc, lds, R->partial, base + o_h1, lds,
-                          R->counters + S, s));
-    }
-    {
-      ProfScope ps(K_CGS_UPDATE, s);
-      CPM_TRY(launch_cgs_update(Sg, kk, R->V, R->ldv, R->W, base + o_sc, lds, base + o_h1, R->partial,
-                                base + o_h2, lds, R->counters + 2 * S, s));
-    }
-    {
-      ProfScope ps(K_CGS_FINAL, s);
-      CPM_TRY(launch_cgs_final(Sg, kk, R->V, R->ldv, R->W, base + o_sc, lds, base + o_h2, lds,
-                               R->V + (size_t)(j + 1) * R->ldv, R->partial, base + o_nrm2, lds,
-                               R->counters + 3 * S, s));
+      CPM_TRY(launch_dcgs_dots(Sg, j + 1, R->V, R->ldv, R->W, R->partial, 2 * (kMaxInner + 2) + 8,
+                               base + o_red, lds, R->counters + S, s));
     }
     {
       ProfScope ps(K_OTHER, s);
-      k_inner_step<<<1, 64, 0, s>>>(st, S, j);
+      k_inner_dcgs_step<<<S, kInnerStepThreads, 0, s>>>(st, j);
       count_launch();
+    }
+    if (j < k) {
+      ProfScope ps(K_CGS_UPDATE, s);
+      CPM_TRY(launch_dcgs_update(Sg, j + 1, R->V, R->ldv, R->W, base + o_coef, kMaxInner + 2, lds, s));
     }
   }
   {
@@ -683,7 +745,7 @@ int ras_apply_device(const cpm_ras* ras, const double* r, double* z, cudaStream_
     k_inner_lsq<<<S, 32, 0, s>>>(st);
     count_launch();
     const int* kks = (const int*)((const char*)st + offsetof(InnerState, kk));
-    vec::k_combine<<<grid, VB, 0, s>>>(Sg, R->V, R->ldv, base + o_y, lds, base + o_sc, lds, kks,
+    vec::k_combine<<<grid, VB, 0, s>>>(Sg, R->V, R->ldv, base + o_y, lds, nullptr, 0, kks,
                                        (int)(sizeof(InnerState) / sizeof(int)), 0, R->lo, R->hi,
                                        R->xoff, z, 0);
     count_launch();

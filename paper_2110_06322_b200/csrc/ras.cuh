@@ -20,9 +20,14 @@ struct InnerState {
   double cs[kMaxInner], sn[kMaxInner];
   double g[kMaxInner + 1], y[kMaxInner];
   double sc[kMaxInner + 2];
-  double h1[kMaxInner + 2], h2[kMaxInner + 2];
   double beta2, nrm2;
   int kk, pad_;
+  // delayed CGS2 (vecops.cuh): unrotated columns, pending first projection,
+  // reductions [<Q_i,u_j>, <u_j,u_j> | <Q_i,z>, <u_j,z>], update coefficients b, e, rho, mu
+  double Hr[(kMaxInner + 1) * kMaxInner];
+  double cpend[kMaxInner + 2];
+  double red[2 * (kMaxInner + 2)];
+  double coef[2 * (kMaxInner + 2) + 2];
 };
 static_assert(sizeof(InnerState) % sizeof(double) == 0, "InnerState stride");
 // z = M r; r_halo: received RAS-halo values (distributed RAS; null: the internal buffer)

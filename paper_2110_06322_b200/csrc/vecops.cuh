@@ -258,7 +258,8 @@ static __global__ void __launch_bounds__(TB) k_proj(Seg S, int k, const double* 
 //   k_dcgs_dots:   out[i] = <col_i, u_j>,  out[k + i] = <col_i, z>   (i < k)
 //   k_dcgs_update: V_j <- (u_j - sum_i b_i Q_i) / rho
 //                  V_{j+1} <- (z - mu u_j - sum_i e_i Q_i) / rho
-//   (b = coef[0..j), e = coef[ldc .. ldc + j), rho = coef[2 ldc], mu = coef[2 ldc + 1])
+//   (b = coef[0..j), e = coef[ldc .. ldc + j), rho = coef[2 ldc], mu = coef[2 ldc + 1];
+//   segment s reads coef + s * cstride)
 template <int TB>
 static __global__ void __launch_bounds__(TB) k_dcgs_dots(Seg S, int k, const double* __restrict__ V,
                                                          int64_t ldv, const double* __restrict__ z,
@@ -326,7 +327,8 @@ static __global__ void __launch_bounds__(TB) k_dcgs_dots(Seg S, int k, const dou
 template <int TB>
 static __global__ void __launch_bounds__(TB) k_dcgs_update(Seg S, int k, double* V, int64_t ldv,
                                                            const double* __restrict__ z,
-                                                           const double* __restrict__ coef, int ldc) {
+                                                           const double* __restrict__ coef0, int ldc,
+                                                           int64_t cstride) {
   constexpr int SV = TB + 4;
   extern __shared__ double smp[];
   double* sv = smp;             // k columns of SV
@@ -334,6 +336,7 @@ static __global__ void __launch_bounds__(TB) k_dcgs_update(Seg S, int k, double*
   double* ce = cb + k;
   const int s = blockIdx.x / S.gps, lb = blockIdx.x % S.gps;
   const int64_t o0 = S.off[s], n = S.off[s + 1] - o0;
+  const double* coef = coef0 + (size_t)s * cstride;  // this segment's coefficients
   const int tid = threadIdx.x;
   const int j = k - 1;
   for (int i = tid; i < j; i += TB) {
@@ -512,5 +515,11 @@ int launch_cgs_update(const vec::Seg& S, int k, const double* V, int64_t ldv, do
 int launch_cgs_final(const vec::Seg& S, int k, const double* V, int64_t ldv, const double* w,
                      const double* sc, int lds, const double* coef, int ldo, double* vout,
                      double* partial, double* out, int ldn, unsigned* counters, cudaStream_t st);
+// delayed CGS2 passes (k = j + 1 columns: Q_0..Q_{j-1} and the lagged u_j)
+int launch_dcgs_dots(const vec::Seg& S, int k, const double* V, int64_t ldv, const double* z,
+                     double* partial, int pld, double* out, int ldo, unsigned* counters,
+                     cudaStream_t st);
+int launch_dcgs_update(const vec::Seg& S, int k, double* V, int64_t ldv, const double* z,
+                       const double* coef, int ldc, int64_t cstride, cudaStream_t st);
 
 }  // namespace cpm
