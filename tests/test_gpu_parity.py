@@ -49,7 +49,9 @@ def _gpu_band(cpm, kind, h, **kw):
 
 
 CASES = [("sphere", 0.1, {}), ("sphere", 0.13, {}), ("torus", 0.05, {"R": 1.0, "r": 0.4}),
-         ("sphere", 0.06, {"R": 0.7})]
+         ("sphere", 0.06, {"R": 0.7}),
+         ("sphere", 0.19, {}),  # coarsest spacing with lambda + h < reach: sparse, ragged tiles
+         ("sphere", 0.1, {"L": 1.2})]  # band clipped by the box [-L, L]^3 (stencils still inside)
 
 
 def _oracle_surface(kind, kw):
@@ -59,7 +61,7 @@ def _oracle_surface(kind, kw):
 @pytest.mark.parametrize("kind,h,kw", CASES)
 def test_band_bit_exact(cpm, kind, h, kw):
     gb = _gpu_band(cpm, kind, h, **kw)
-    ob = OBand(_oracle_surface(kind, kw), h)
+    ob = OBand(_oracle_surface(kind, kw), h, L=kw.get("L", 2.0))
     ga = cpm.cpm_band_active_coords(gb).astype(np.int64)
     gg = cpm.cpm_band_ghost_coords(gb).astype(np.int64)
     assert gb.info.n_active == ob.nA and gb.info.n_ghost == ob.nG
@@ -74,7 +76,7 @@ def test_band_bit_exact(cpm, kind, h, kw):
 @pytest.mark.parametrize("c", [1.0, 10.0])
 def test_apply_parity(cpm, kind, h, kw, c):
     gb = _gpu_band(cpm, kind, h, **kw)
-    ob = OBand(_oracle_surface(kind, kw), h)
+    ob = OBand(_oracle_surface(kind, kw), h, L=kw.get("L", 2.0))
     ga = cpm.cpm_band_active_coords(gb).astype(np.int64)
     perm = _perm_to_oracle(ga, ob)
     u_h = seeded_inputs.uniform_pm1(0, ga)
@@ -126,6 +128,13 @@ def test_band_errors(cpm):
         cpm.cpm_build_band("sphere", 0.1, L=0.3)           # box misses the surface
     with pytest.raises(cpm.CpmError, match="p = 3"):
         cpm.cpm_build_band("sphere", 0.1, p=2)
+    # box clipping the band so that stencils leave Sigma_A: both sides refuse
+    with pytest.raises(cpm.CpmError, match="StencilEscape"):
+        cpm.cpm_build_band("sphere", 0.1, L=1.1)
+    from oracle.interp import extension_matrix
+
+    with pytest.raises(ValueError, match="StencilEscape"):
+        extension_matrix(OBand(Sphere(1.0), 0.1, L=1.1))
 
 
 def test_solve_parity_config0(cpm):
