@@ -230,9 +230,9 @@ def run_mine(args):
             prof[phase][k] = (a + ms, b + n)
         cpm.cpm_profile_reset()
 
-    def step(record):
+    def step(record, profile=False):
         evs = []
-        if record is not None:
+        if profile:
             cpm.cpm_profile_reset()
             cpm.cpm_profile_enable(True)
         for _ in range(CFG["applies"]):
@@ -242,7 +242,7 @@ def run_mine(args):
             cpm.cpm_apply(band, c, u, y)
             b.record(stream)
             evs.append((a, b))
-        if record is not None:
+        if profile:
             take_profile("apply")
         x.zero_()
         sa = torch.cuda.Event(enable_timing=True)
@@ -250,9 +250,10 @@ def run_mine(args):
         sa.record(stream)
         st = cpm.cpm_solve(band, c, f, x, rtol=CFG["rtol"], restart=CFG["restart"])
         sb.record(stream)
-        if record is not None:
+        if profile:
             take_profile("solve")
             cpm.cpm_profile_enable(False)
+        if record is not None:
             record.append((evs, (sa, sb), st))
 
     for _ in range(args.warmup):
@@ -277,6 +278,10 @@ def run_mine(args):
         torch.distributed.barrier()
     launches = cpm.cpm_kernel_launches() - launches0
     clk = clocks.stop()
+    # one more (untimed) step with per-kernel CUDA events: the kernel breakdown and
+    # the per-launch times of the roofline (the timed steps run without them)
+    step(None, profile=True)
+    torch.cuda.synchronize()
     total_ms = ga.elapsed_time(gb)
     apply_ms = sum(a.elapsed_time(b) for evs, _, _ in rec for a, b in evs)
     solve_ms = [sa.elapsed_time(sb) for _, (sa, sb), _ in rec]
@@ -336,7 +341,8 @@ def run_mine(args):
 
     peak, peak_src = _peaks()
     alg_bytes = 16 * nA + 28 * nE          # u + y + (t_xyz + eoff) per eval node
-    mean_apply_s = (ext_ms + lap_ms) / 1e3 / max(ext_n, 1)
+    # per apply (2 launches) over the timed region, CUDA events on the launching stream
+    mean_apply_s = apply_ms / 1e3 / (CFG["applies"] * args.steps)
     achieved = alg_bytes / mean_apply_s / 1e9
     traffic = _traffic()
     # Krylov passes of the solve (delayed CGS2): per Arnoldi step j one reduction
@@ -350,7 +356,7 @@ def run_mine(args):
         for j in range(steps + 1):          # + the final reduction of the cycle
             kry_bytes += 8 * nA * ((j + 2) + ((j + 4) if j < steps else 0))
         left -= steps
-    kry_ms = sum(prof["solve"][k][0] for k in ("mdot", "cgs_update", "cgs_final")) / args.steps
+    kry_ms = sum(prof["solve"][k][0] for k in ("mdot", "cgs_update", "cgs_final"))
     kry_gbs = kry_bytes / (kry_ms / 1e3) / 1e9 if kry_ms > 0 else None
     if rank == 0:
         cpu_rate, cpu_s, cores = (None, None, None)
@@ -372,6 +378,7 @@ def run_mine(args):
                          "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                          "alg_bytes_per_apply": alg_bytes,
+                         "apply_ms": mean_apply_s * 1e3,
                          "extend_ms": ext_ms / max(ext_n, 1), "laplace_ms": lap_ms / max(lap_n, 1),
                          "note": "extend is bound by shared-memory gathers (DESIGN.md §Kernels); "
                                  "traffic = ncu DRAM bytes per apply (profiles/r01_traffic.json)"},
@@ -380,7 +387,7 @@ def run_mine(args):
                                "bound": "hbm", "achieved": kry_gbs, "peak": peak, "unit": "GB/s",
                                "frac": (kry_gbs / peak) if kry_gbs else None,
                                "alg_bytes_per_solve": kry_bytes, "ms_per_solve": kry_ms},
-            "kernels_ms_per_step": {ph: {k: v[0] / args.steps for k, v in d.items() if v[1]}
+            "kernels_ms_per_step": {ph: {k: v[0] for k, v in d.items() if v[1]}
                                     for ph, d in prof.items()},
             "cpu_baseline": ({"value": cpu_rate, "unit": UNIT, "cores": cores, "kind": "oracle",
                               "sample": f"{args.cpu_rows} sampled active rows of config 1, "

@@ -141,7 +141,9 @@ __global__ void __launch_bounds__(kNtThreads, 8)
                 const uint64_t* __restrict__ runs, const double* __restrict__ u,
                 const double* __restrict__ uh, uint32_t split, const double* __restrict__ tx,
                 const double* __restrict__ ty, const double* __restrict__ tz,
-                const uint32_t* __restrict__ eoff, double* __restrict__ vb) {
+                const uint32_t* __restrict__ eoff, double* __restrict__ vb,
+                const int* __restrict__ skip) {
+  if (skip && *skip) return;
   extern __shared__ double smn[];
   double* box = smn;
   uint64_t* desc = (uint64_t*)(box + boxCells);
@@ -223,7 +225,9 @@ __global__ void __launch_bounds__(kLapThreads) k_laplace(const TileHdr* __restri
                                                          const double* __restrict__ vb,
                                                          double* __restrict__ y, double diag,
                                                          double ih2,
-                                                         const double* __restrict__ scale, int lds) {
+                                                         const double* __restrict__ scale, int lds,
+                                                         const int* __restrict__ skip) {
+  if (skip && *skip) return;
   __shared__ double E[1000];
   const int t = blockIdx.x, tid = threadIdx.x;
   const TileHdr* T = tiles + t;
@@ -295,12 +299,12 @@ __global__ void __launch_bounds__(kLapThreads) k_laplace(const TileHdr* __restri
 }  // namespace
 
 int apply_device(const cpm_band* b, double c, const double* u, double* y, const double* scale,
-                 int lds, cudaStream_t s) {
-  return apply_device_split(b, c, u, u, y, scale, lds, s);
+                 int lds, cudaStream_t s, const int* skip) {
+  return apply_device_split(b, c, u, u, y, scale, lds, s, skip);
 }
 
 int apply_device_split(const cpm_band* b, double c, const double* u, const double* uh, double* y,
-                       const double* scale, int lds, cudaStream_t s) {
+                       const double* scale, int lds, cudaStream_t s, const int* skip) {
   const double ih2 = 1.0 / (b->h * b->h);
   const double diag = c + 6.0 * ih2;
   {
@@ -317,7 +321,7 @@ int apply_device_split(const cpm_band* b, double c, const double* u, const doubl
     }                                                                                        \
     k_extend_nt<Z><<<b->nT, kNtThreads, smem, s>>>(b->tiles, b->maxBox, descCap, b->runs, u, uh, \
                                                    b->srcSplit, b->tx, b->ty, b->tz, b->eoff,   \
-                                                   b->vb);                                      \
+                                                   b->vb, skip);                                \
   } while (0)
     if (b->zeroFill) CPM_EXTNT(true); else CPM_EXTNT(false);
 #undef CPM_EXTNT
@@ -326,7 +330,7 @@ int apply_device_split(const cpm_band* b, double c, const double* u, const doubl
   {
     ProfScope ps(K_LAPLACE, s);
     // 128 threads per tile: 16 resident tiles per SM keep enough loads in flight
-    k_laplace<128><<<b->nT, 128, 0, s>>>(b->tiles, u, b->acell, b->vb, y, diag, ih2, scale, lds);
+    k_laplace<128><<<b->nT, 128, 0, s>>>(b->tiles, u, b->acell, b->vb, y, diag, ih2, scale, lds, skip);
     count_launch();
   }
   CPM_CUDA(cudaGetLastError());

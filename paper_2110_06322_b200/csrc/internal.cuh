@@ -136,11 +136,13 @@ namespace cpm {
 // apply.cu
 // y = scale_seg * (c - Delta_S^h) u ; scale (device, may be null) is read at
 // scale[seg * lds] with seg = the tile's segment id (0 for a plain band).
+// skip (device, may be null): when *skip != 0 at kernel start the kernels return
+// without work (GMRES steps queued past convergence).
 int apply_device(const cpm_band* b, double c, const double* u, double* y, const double* scale,
-                 int lds, cudaStream_t s);
+                 int lds, cudaStream_t s, const int* skip = nullptr);
 // as apply_device, with fill-run sources >= b->srcSplit read from uh[src - srcSplit]
 int apply_device_split(const cpm_band* b, double c, const double* u, const double* uh, double* y,
-                       const double* scale, int lds, cudaStream_t s);
+                       const double* scale, int lds, cudaStream_t s, const int* skip = nullptr);
 // build.cu
 int build_band(const cpm_surface* surf, double h, int p, double L, cudaStream_t s, cpm_band** out);
 void free_band(cpm_band* b);

@@ -93,6 +93,7 @@ int launch_cgs_update(const vec::Seg& S, int k, const double* V, int64_t ldv, do
 
 namespace {
 constexpr int kLdc = kMaxRestart + 2;  // stride of GState::coef / red halves
+constexpr int kHostCheck = 8;          // DCGS2 steps queued between host looks at st->done
 // unpreconditioned GMRES uses delayed CGS2 (2 passes per step); CPM_CGS2=1 forces
 // the 3-pass CGS2 of the flexible path (A/B measurements)
 const bool g_force_cgs2 = [] {
@@ -103,7 +104,7 @@ const bool g_force_cgs2 = [] {
 
 int launch_dcgs_dots(const vec::Seg& S, int k, const double* V, int64_t ldv, const double* z,
                      double* partial, int pld, double* out, int ldo, unsigned* counters,
-                     cudaStream_t st) {
+                     cudaStream_t st, const int* skip) {
   const int grid = S.nseg * S.gps;
   if (k <= 64) {
     const size_t sm = ((size_t)k * (256 + 4) + 256) * sizeof(double);
@@ -113,7 +114,7 @@ int launch_dcgs_dots(const vec::Seg& S, int k, const double* V, int64_t ldv, con
                                     (int)(((size_t)64 * 260 + 256) * sizeof(double))));
       attr = true;
     }
-    vec::k_dcgs_dots<256><<<grid, 256, sm, st>>>(S, k, V, ldv, z, partial, pld, out, ldo, counters);
+    vec::k_dcgs_dots<256><<<grid, 256, sm, st>>>(S, k, V, ldv, z, partial, pld, out, ldo, counters, skip);
   } else {
     static bool attr = false;
     const size_t sm2 = ((size_t)k * (128 + 4) + 128) * sizeof(double);
@@ -122,7 +123,7 @@ int launch_dcgs_dots(const vec::Seg& S, int k, const double* V, int64_t ldv, con
                                     (int)(((size_t)(kMaxRestart + 1) * 132 + 128) * sizeof(double))));
       attr = true;
     }
-    vec::k_dcgs_dots<128><<<grid, 128, sm2, st>>>(S, k, V, ldv, z, partial, pld, out, ldo, counters);
+    vec::k_dcgs_dots<128><<<grid, 128, sm2, st>>>(S, k, V, ldv, z, partial, pld, out, ldo, counters, skip);
   }
   count_launch();
   CPM_CUDA(cudaGetLastError());
@@ -130,7 +131,8 @@ int launch_dcgs_dots(const vec::Seg& S, int k, const double* V, int64_t ldv, con
 }
 
 int launch_dcgs_update(const vec::Seg& S, int k, double* V, int64_t ldv, const double* z,
-                       const double* coef, int ldc, int64_t cstride, cudaStream_t st) {
+                       const double* coef, int ldc, int64_t cstride, cudaStream_t st,
+                       const int* skip) {
   const int grid = S.nseg * S.gps;
   if (k <= 64) {
     const size_t sm = ((size_t)k * (256 + 4) + 2 * (size_t)k) * sizeof(double);
@@ -140,7 +142,7 @@ int launch_dcgs_update(const vec::Seg& S, int k, double* V, int64_t ldv, const d
                                     (int)(((size_t)64 * 260 + 128) * sizeof(double))));
       attr = true;
     }
-    vec::k_dcgs_update<256><<<grid, 256, sm, st>>>(S, k, V, ldv, z, coef, ldc, cstride);
+    vec::k_dcgs_update<256><<<grid, 256, sm, st>>>(S, k, V, ldv, z, coef, ldc, cstride, skip);
   } else {
     const size_t sm = ((size_t)k * (128 + 4) + 2 * (size_t)k) * sizeof(double);
     static bool attr = false;
@@ -149,7 +151,7 @@ int launch_dcgs_update(const vec::Seg& S, int k, double* V, int64_t ldv, const d
                                     (int)(((size_t)(kMaxRestart + 1) * 132 + 2 * (kMaxRestart + 1)) * sizeof(double))));
       attr = true;
     }
-    vec::k_dcgs_update<128><<<grid, 128, sm, st>>>(S, k, V, ldv, z, coef, ldc, cstride);
+    vec::k_dcgs_update<128><<<grid, 128, sm, st>>>(S, k, V, ldv, z, coef, ldc, cstride, skip);
   }
   count_launch();
   CPM_CUDA(cudaGetLastError());
@@ -214,7 +216,8 @@ __global__ void k_arnoldi_step(GState* st, int j, int m) {
 // and the next lagged vector u_{j+1} = (z - mu u_j - Q (d - mu b))/rho
 // (k_dcgs_update, coefficients in st->coef).
 constexpr int kStepThreads = 128;
-__global__ void __launch_bounds__(kStepThreads) k_dcgs_step(GState* st, int j, int m) {
+__global__ void __launch_bounds__(kStepThreads) k_dcgs_step(GState* st, int j, int m, int maxit) {
+  if (st->done) return;  // a step queued past convergence
   const int ld = kMaxRestart + 1, k = j + 1, tid = threadIdx.x;
   const double* b = st->red;
   const double* d = st->red + k;
@@ -277,7 +280,7 @@ __global__ void __launch_bounds__(kStepThreads) k_dcgs_step(GState* st, int j, i
       st->k = j;
       st->its += 1;
       st->breakdown = brk;
-      if (st->est <= st->target || brk || j == m) sdone = 1;
+      if (st->est <= st->target || brk || j == m || st->its >= maxit) sdone = 1;
     }
     if (sdone) st->done = 1;
   }
@@ -416,7 +419,7 @@ int gmres_device(const LinOp& A, const PrecOp* M, const double* b, double* x, in
   }
   while (!converged) {
     // r = b - A x  -> V_0 ; beta
-    CPM_TRY(A.apply(x, ws.t, nullptr, s));
+    CPM_TRY(A.apply(x, ws.t, nullptr, nullptr, s));
     {
       ProfScope ps(K_AXPY, s);
       vec::k_sub_nrm2<<<G, VB, 0, s>>>(S, b, ws.t, ws.V, ws.partial, &st->beta2, 0, cnt);
@@ -440,26 +443,34 @@ int gmres_device(const LinOp& A, const PrecOp* M, const double* b, double* x, in
         vec::k_scale<<<G, VB, 0, s>>>(S, ws.V, st->sc, 0, 0, ws.V);
         count_launch();
       }
+      // Steps are queued without a host round trip; st->done (set by the step
+      // kernel at convergence, breakdown, the end of the cycle or maxit) turns the
+      // kernels of steps queued past it into no-ops.  The host looks every
+      // kHostCheck steps only to stop queueing.
+      const int* skip = &st->done;
       for (int j = 0; j <= m; ++j) {
         double* Vj = ws.V + (size_t)j * ws.ldv;
-        if (j < m) CPM_TRY(A.apply(Vj, ws.w, nullptr, s));  // z = A u_j
+        if (j < m) CPM_TRY(A.apply(Vj, ws.w, nullptr, skip, s));  // z = A u_j
         const int k = j + 1;
         {
           ProfScope ps(K_MDOT, s);
-          CPM_TRY(launch_dcgs_dots(S, k, ws.V, ws.ldv, ws.w, ws.partial, 2 * kLdc + 8, st->red, 0, cnt + 1, s));
+          CPM_TRY(launch_dcgs_dots(S, k, ws.V, ws.ldv, ws.w, ws.partial, 2 * kLdc + 8, st->red, 0, cnt + 1,
+                                   s, skip));
           CPM_TRY(allreduce(st->red, 2 * k));
         }
         {
           ProfScope ps(K_OTHER, s);
-          k_dcgs_step<<<1, kStepThreads, 0, s>>>(st, j, m);
+          k_dcgs_step<<<1, kStepThreads, 0, s>>>(st, j, m, maxit);
           count_launch();
         }
-        CPM_TRY(fetch_state(ws, s));
-        its = ws.hst->its;
-        if (ws.hst->done || its >= maxit) break;
-        {
+        if (j < m) {
           ProfScope ps(K_CGS_UPDATE, s);
-          CPM_TRY(launch_dcgs_update(S, k, ws.V, ws.ldv, ws.w, st->coef, kLdc, 0, s));
+          CPM_TRY(launch_dcgs_update(S, k, ws.V, ws.ldv, ws.w, st->coef, kLdc, 0, s, skip));
+        }
+        if ((j + 1) % kHostCheck == 0 || j == m) {
+          CPM_TRY(fetch_state(ws, s));
+          its = ws.hst->its;
+          if (ws.hst->done) break;
         }
       }
     } else
@@ -473,9 +484,9 @@ int gmres_device(const LinOp& A, const PrecOp* M, const double* b, double* x, in
         }
         double* Zj = ws.Z + (size_t)j * ws.ldv;
         CPM_TRY(M->apply(ws.w, Zj, s));
-        CPM_TRY(A.apply(Zj, ws.w, nullptr, s));
+        CPM_TRY(A.apply(Zj, ws.w, nullptr, nullptr, s));
       } else {
-        CPM_TRY(A.apply(Vj, ws.w, &st->sc[j], s));
+        CPM_TRY(A.apply(Vj, ws.w, &st->sc[j], nullptr, s));
       }
       const int k = j + 1;
       {
@@ -527,7 +538,7 @@ int gmres_device(const LinOp& A, const PrecOp* M, const double* b, double* x, in
   }
   double rtrue = 0.0;
   if (stats) {
-    CPM_TRY(A.apply(x, ws.t, nullptr, s));
+    CPM_TRY(A.apply(x, ws.t, nullptr, nullptr, s));
     {
       ProfScope ps(K_OTHER, s);
       vec::k_sub_nrm2<<<G, VB, 0, s>>>(S, b, ws.t, nullptr, ws.partial, &st->beta2, 0, cnt);

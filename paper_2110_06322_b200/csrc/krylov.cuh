@@ -36,9 +36,10 @@ struct HostState {
   double est, beta2;
 };
 
-// y = scale * A x  (scale: device pointer or nullptr)
+// y = scale * A x  (scale: device pointer or nullptr; skip: device flag, kernels
+// return without work when it is set — GMRES steps queued past convergence)
 struct LinOp {
-  std::function<int(const double*, double*, const double*, cudaStream_t)> apply;
+  std::function<int(const double*, double*, const double*, const int*, cudaStream_t)> apply;
   // sum-allreduce of n device doubles across ranks (empty on one GPU)
   std::function<int(double*, size_t, cudaStream_t)> allreduce;
 };

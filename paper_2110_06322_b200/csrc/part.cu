@@ -516,9 +516,10 @@ int cpm_part_solve(const cpm_part* p, const cpm_comm* comm, double c, const doub
     };
   }
   LinOp A;
-  A.apply = [p, comm, c](const double* x, double* y, const double* scale, cudaStream_t st) {
-    CPM_TRY(part_exchange(p, comm, x, st));
-    return apply_device_split(&p->lb, c, x, p->hbuf, y, scale, 0, st);
+  A.apply = [p, comm, c](const double* x, double* y, const double* scale, const int* skip,
+                         cudaStream_t st) {
+    CPM_TRY(part_exchange(p, comm, x, st));  // collective: always performed
+    return apply_device_split(&p->lb, c, x, p->hbuf, y, scale, 0, st, skip);
   };
   A.allreduce = [comm](double* buf, size_t n, cudaStream_t st) { return comm_allreduce_sum(comm, buf, n, st); };
   cpm_solve_stats local;

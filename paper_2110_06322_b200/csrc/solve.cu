@@ -21,8 +21,8 @@ extern "C" int cpm_solve(const cpm_band* b, double c, const double* f, double* u
   if (maxit < 0) return fail(CPM_ERR_ARG, "cpm_solve: maxit must be >= 0");
   cudaStream_t s = (cudaStream_t)stream;
   LinOp A;
-  A.apply = [b, c](const double* x, double* y, const double* scale, cudaStream_t st) {
-    return apply_device(b, c, x, y, scale, 0, st);
+  A.apply = [b, c](const double* x, double* y, const double* scale, const int* skip, cudaStream_t st) {
+    return apply_device(b, c, x, y, scale, 0, st, skip);
   };
   PrecOp M;
   if (ras) {
@@ -101,8 +101,8 @@ extern "C" int cpm_rd_step(const cpm_band* b, const cpm_rd_params* p, double* u,
   for (int q = 0; q < 2; ++q) {
     const double c = q == 0 ? c1 : c2;
     LinOp A;
-    A.apply = [b, c](const double* x, double* y, const double* scale, cudaStream_t st) {
-      return apply_device(b, c, x, y, scale, 0, st);
+    A.apply = [b, c](const double* x, double* y, const double* scale, const int* skip, cudaStream_t st) {
+      return apply_device(b, c, x, y, scale, 0, st, skip);
     };
     CPM_TRY(gmres_device(A, nullptr, q == 0 ? mb->dstage0 : mb->dstage1, q == 0 ? u : v, b->nA, p->rtol,
                          p->restart, p->maxit, band_ws(b), q == 0 ? (su ? su : &l1) : (sv ? sv : &l2), s));

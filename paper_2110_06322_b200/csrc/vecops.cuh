@@ -264,7 +264,9 @@ template <int TB>
 static __global__ void __launch_bounds__(TB) k_dcgs_dots(Seg S, int k, const double* __restrict__ V,
                                                          int64_t ldv, const double* __restrict__ z,
                                                          double* partial, int pld, double* out,
-                                                         int ldo, unsigned* counters) {
+                                                         int ldo, unsigned* counters,
+                                                         const int* __restrict__ skip) {
+  if (skip && *skip) return;
   constexpr int SV = TB + 4;
   extern __shared__ double smp[];
   double* sv = smp;             // k columns of SV
@@ -328,7 +330,8 @@ template <int TB>
 static __global__ void __launch_bounds__(TB) k_dcgs_update(Seg S, int k, double* V, int64_t ldv,
                                                            const double* __restrict__ z,
                                                            const double* __restrict__ coef0, int ldc,
-                                                           int64_t cstride) {
+                                                           int64_t cstride, const int* __restrict__ skip) {
+  if (skip && *skip) return;
   constexpr int SV = TB + 4;
   extern __shared__ double smp[];
   double* sv = smp;             // k columns of SV
@@ -518,8 +521,9 @@ int launch_cgs_final(const vec::Seg& S, int k, const double* V, int64_t ldv, con
 // delayed CGS2 passes (k = j + 1 columns: Q_0..Q_{j-1} and the lagged u_j)
 int launch_dcgs_dots(const vec::Seg& S, int k, const double* V, int64_t ldv, const double* z,
                      double* partial, int pld, double* out, int ldo, unsigned* counters,
-                     cudaStream_t st);
+                     cudaStream_t st, const int* skip = nullptr);
 int launch_dcgs_update(const vec::Seg& S, int k, double* V, int64_t ldv, const double* z,
-                       const double* coef, int ldc, int64_t cstride, cudaStream_t st);
+                       const double* coef, int ldc, int64_t cstride, cudaStream_t st,
+                       const int* skip = nullptr);
 
 }  // namespace cpm

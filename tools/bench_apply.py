@@ -59,3 +59,10 @@ if os.environ.get("CPM_SOLVE"):
     cpm.cpm_profile_enable(False)
     out = {k: cpm.cpm_profile_read(k) for k in ["extend", "laplace", "mdot", "cgs_update", "cgs_final", "axpy", "other"]}
     print("solve 200 its:", f"{st.seconds:.3f}s", {k: f"{v[0]:.1f}ms/{v[1]}" for k, v in out.items()})
+    for _ in range(2):
+        x.zero_()
+        st = cpm.cpm_solve(band, 10.0, f, x, rtol=1e-10, restart=50, maxit=200)
+        print("solve 200 its, profiling off:", f"{st.seconds:.3f}s")
+    x.zero_()
+    st = cpm.cpm_solve(band, 10.0, f, x, rtol=1e-10, restart=50)
+    print("full solve, profiling off:", f"{st.seconds:.3f}s", st.iterations, "its")
