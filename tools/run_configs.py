@@ -1,7 +1,9 @@
-"""Full-size BASELINE configs 2 and 3 on one GPU: band build, RAS set-up, RAS-FGMRES(50)
-solve; prints one JSON line per config (timings, iterations, true residual).
+"""Full-size BASELINE configs on the GPU: band build, RAS set-up, RAS-FGMRES(50) solve
+(configs 2, 3), Schnakenberg IMEX steps (config 4); one JSON line per run.
 
-usage: python tools/run_configs.py [2] [3]      (default: both)
+usage: python tools/run_configs.py [2] [3] [4] [--k 16] [--h H] [--nsub 8]
+       torchrun --nproc-per-node N --master-addr 127.0.0.1 tools/run_configs.py 2 --dist
+         (config 2 / 3 partitioned over N GPUs: NCCL halo + distributed RAS + FGMRES)
 """
 import json
 import os
@@ -75,6 +77,52 @@ def run_rd(h=1.0 / 400, steps=200):
             "v_range": [float(v.min()), float(v.max())]}
 
 
+def run_dist(cfg: int, k_inner: int = 16, restart: int = 50, maxit: int = 20000, h=None, nsub: int = 8):
+    """Config 2 / 3 partitioned over the ranks of a torchrun job (one GPU each): Morton
+    slabs, NCCL halo exchange, distributed RAS (nsub a multiple of the rank count),
+    distributed FGMRES; prints the max-over-ranks solve time on rank 0."""
+    import torch.distributed as dist
+
+    from paper_2110_06322_b200.distributed import DistributedCPM
+
+    dist.init_process_group("nccl")
+    rank, nr = dist.get_rank(), dist.get_world_size()
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", rank)))
+    if cfg == 2:
+        band = cpm.cpm_build_band("torus", h or 1.0 / 400, R=1.0, r=0.4)
+        c = 1.0
+    else:
+        band = cpm.cpm_build_band("sphere", h or 1.0 / 800)
+        c = 0.1
+    f = torch.empty(band.n, dtype=torch.float64, device="cuda")
+    if cfg == 2:
+        cpm.cpm_eval_torus_rhs(band, seeded_inputs.smooth_modulation_coeffs(1), f)
+    else:
+        cpm.cpm_eval_sph(band, 10, 5, 1.0, f)
+        ga = cpm.cpm_band_active_coords(band).astype(np.int64)
+        f += torch.from_numpy(1e-3 * seeded_inputs.normal(2, ga)).cuda()
+    D = DistributedCPM(band)
+    ras = D.setup_ras(nsub, 4, k_inner, c)
+    fo = f[D.lo:D.hi].contiguous()
+    uo = torch.zeros_like(fo)
+    dist.barrier()
+    torch.cuda.synchronize()
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    a.record()
+    st = D.solve(c, fo, uo, rtol=1e-10, restart=restart, maxit=maxit, ras=ras)
+    b.record()
+    torch.cuda.synchronize()
+    t = torch.tensor([a.elapsed_time(b) / 1e3], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        print(json.dumps({"config": cfg, "ranks": nr, "n_active": band.n, "nsub": nsub, "k_inner": k_inner,
+                          "solve_s_max_over_ranks": float(t.item()), "iterations": st.iterations,
+                          "converged": bool(st.converged), "resid_true_rel": st.resid_true / st.bnorm}),
+              flush=True)
+    dist.destroy_process_group()
+
+
 if __name__ == "__main__":
     import argparse
 
@@ -85,7 +133,13 @@ if __name__ == "__main__":
     ap.add_argument("--nsub", type=int, default=8)
     ap.add_argument("--maxit", type=int, default=20000)
     ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--dist", action="store_true",
+                    help="partitioned solve under torchrun (one rank per GPU, NCCL)")
     a = ap.parse_args()
+    if a.dist:
+        for c in a.configs:
+            run_dist(c, k_inner=a.k[0], h=a.h, nsub=a.nsub, maxit=a.maxit)
+        sys.exit(0)
     if 4 in a.configs:
         print(json.dumps(run_rd(h=a.h or 1.0 / 400, steps=a.steps)), flush=True)
     for c in [c for c in a.configs if c != 4]:
