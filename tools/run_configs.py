@@ -18,7 +18,8 @@ import paper_2110_06322_b200 as cpm
 import seeded_inputs
 
 
-def run(cfg: int, k_inner: int = 8, restart: int = 50, maxit: int = 20000, h=None, nsub: int = 8):
+def run(cfg: int, k_inner: int = 8, restart: int = 50, maxit: int = 20000, h=None, nsub: int = 8,
+        overlap: int = 4):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     if cfg == 2:
@@ -38,7 +39,7 @@ def run(cfg: int, k_inner: int = 8, restart: int = 50, maxit: int = 20000, h=Non
         ga = cpm.cpm_band_active_coords(band).astype(np.int64)
         f += torch.from_numpy(1e-3 * seeded_inputs.normal(2, ga)).cuda()
     t0 = time.perf_counter()
-    ras = cpm.cpm_ras_setup(band, nsub, 4, k_inner, c) if k_inner > 0 else None
+    ras = cpm.cpm_ras_setup(band, nsub, overlap, k_inner, c) if k_inner > 0 else None
     torch.cuda.synchronize()
     t_ras = time.perf_counter() - t0
     u = torch.zeros_like(f)
@@ -48,7 +49,7 @@ def run(cfg: int, k_inner: int = 8, restart: int = 50, maxit: int = 20000, h=Non
     cpm.cpm_profile_enable(False)
     prof = {k: round(cpm.cpm_profile_read(k)[0], 1) for k in
             ["extend", "laplace", "mdot", "cgs_update", "cgs_final", "axpy", "other"]}
-    return {"config": cfg, "h": band.info.h, "nsub": nsub if k_inner > 0 else 0, "n_active": n, "n_ghost": band.info.n_ghost, "tiles": band.info.n_tiles,
+    return {"config": cfg, "h": band.info.h, "nsub": nsub if k_inner > 0 else 0, "overlap": overlap, "n_active": n, "n_ghost": band.info.n_ghost, "tiles": band.info.n_tiles,
             "build_s": round(t_build, 3), "ras_setup_s": round(t_ras, 3), "k_inner": k_inner,
             "solve_s": round(st.seconds, 3), "iterations": st.iterations, "converged": bool(st.converged),
             "resid_true_rel": st.resid_true / st.bnorm, "ms_per_iteration": round(1e3 * st.seconds / max(st.iterations, 1), 3),
@@ -131,6 +132,7 @@ if __name__ == "__main__":
     ap.add_argument("--h", type=float, default=None, help="override the lattice spacing")
     ap.add_argument("--k", type=int, nargs="*", default=[8], help="inner GMRES steps (0: no RAS)")
     ap.add_argument("--nsub", type=int, default=8)
+    ap.add_argument("--overlap", type=int, nargs="*", default=[4], help="RAS overlap (lattice layers)")
     ap.add_argument("--maxit", type=int, default=20000)
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--dist", action="store_true",
@@ -144,4 +146,6 @@ if __name__ == "__main__":
         print(json.dumps(run_rd(h=a.h or 1.0 / 400, steps=a.steps)), flush=True)
     for c in [c for c in a.configs if c != 4]:
         for k in a.k:
-            print(json.dumps(run(c, k_inner=k, h=a.h, nsub=a.nsub, maxit=a.maxit)), flush=True)
+            for ov in a.overlap:
+                print(json.dumps(run(c, k_inner=k, h=a.h, nsub=a.nsub, maxit=a.maxit, overlap=ov)),
+                      flush=True)
