@@ -207,9 +207,10 @@ __global__ void __launch_bounds__(kNtThreads, 8)
 __device__ __forceinline__ int hidx(int x, int y, int z) { return (x + 1) + 10 * (y + 1) + 100 * (z + 1); }
 
 
-// One CTA per tile.  All global loads (own E u, the neighbours' face layers, the
-// output nodes' u and cells) are issued before the single barrier, so a CTA has
-// one dependent chain: header -> neighbour header -> vb.
+// One CTA per tile.  vb holds E u per brick cell (t * 512 + cell, written by
+// k_extend_nt), so every global load of a CTA is one step from its header:
+// the own eval cells, the neighbours' face layers under own eval cells, and the
+// output nodes' u and cells; then one barrier and the 7-point combination.
 template <int kLapThreads>
 __global__ void __launch_bounds__(kLapThreads) k_laplace(const TileHdr* __restrict__ tiles,
                                                          const double* __restrict__ u,
@@ -237,22 +238,15 @@ __global__ void __launch_bounds__(kLapThreads) k_laplace(const TileHdr* __restri
       au[k] = __ldg(u + a);
     }
   }
-  // own tile: vb slot r (coalesced) -> its cell = the r-th set bit of emask
-  const int ne = T->e1 - T->e0;
+  // own eval cells (the only cells the extend wrote)
   const double* vt = vb + (size_t)t * kBrickCells;
 #pragma unroll
   for (int k = 0; k < kBrickCells / kLapThreads; ++k) {
-    const int r = tid + k * kLapThreads;
-    if (r < ne) {
-      int w = 0;  // last word with epre[w] <= r (epre non-decreasing)
-#pragma unroll
-      for (int st = 8; st > 0; st >>= 1)
-        if (w + st < 16 && T->epre[w + st] <= r) w += st;
-      const int c = 32 * w + (int)__fns(T->emask[w], 0u, r - T->epre[w] + 1);
-      E[hidx(c & 7, (c >> 3) & 7, c >> 6)] = vt[r];
-    }
+    const int c = tid + k * kLapThreads;
+    if ((T->emask[c >> 5] >> (c & 31)) & 1u) E[hidx(c & 7, (c >> 3) & 7, c >> 6)] = __ldg(vt + c);
   }
-  // 6 x 64 face cells of the neighbours (rank lookup in the neighbour's mask)
+  // 6 x 64 face cells of the neighbours, read where the own boundary cell is an eval cell
+  // (every 6-neighbour of an active node is an eval node, Sigma_G of reading R1)
 #pragma unroll
   for (int k = 0; k < (384 + kLapThreads - 1) / kLapThreads; ++k) {
     const int q = tid + k * kLapThreads;
@@ -262,14 +256,13 @@ __global__ void __launch_bounds__(kLapThreads) k_laplace(const TileHdr* __restri
       if (src >= 0) {
         const int axis = f >> 1, plus = (f & 1) == 0;
         const int in = plus ? 0 : 7;    // layer read in the neighbour
+        const int me = plus ? 7 : 0;    // own boundary layer
         const int out = plus ? 8 : -1;  // halo layer written here
-        int c, h;
-        if (axis == 0) { c = in + 8 * i + 64 * j; h = hidx(out, i, j); }
-        else if (axis == 1) { c = i + 8 * in + 64 * j; h = hidx(i, out, j); }
-        else { c = i + 8 * j + 64 * in; h = hidx(i, j, out); }
-        const TileHdr* S = tiles + src;
-        const uint32_t m = S->emask[c >> 5], bit = 1u << (c & 31);
-        if (m & bit) E[h] = vb[(size_t)src * kBrickCells + S->epre[c >> 5] + __popc(m & (bit - 1u))];
+        int c, co, h;
+        if (axis == 0) { c = in + 8 * i + 64 * j; co = me + 8 * i + 64 * j; h = hidx(out, i, j); }
+        else if (axis == 1) { c = i + 8 * in + 64 * j; co = i + 8 * me + 64 * j; h = hidx(i, out, j); }
+        else { c = i + 8 * j + 64 * in; co = i + 8 * j + 64 * me; h = hidx(i, j, out); }
+        if ((T->emask[co >> 5] >> (co & 31)) & 1u) E[h] = __ldg(vb + (size_t)src * kBrickCells + c);
       }
     }
   }

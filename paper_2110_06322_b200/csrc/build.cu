@@ -134,10 +134,6 @@ __global__ void k_compact_tiles(int nb, const int* ne, const int* tslot, const i
     tgm[(size_t)t * 16 + q] = gmask[(size_t)b * 16 + q];
     T.emask[q] = amask[(size_t)b * 16 + q] | gmask[(size_t)b * 16 + q];
   }
-  for (int q = 0, r = 0; q < 16; ++q) {
-    T.epre[q] = (uint16_t)r;
-    r += __popc(T.emask[q]);
-  }
   tiles[t] = T;
 }
 
@@ -295,7 +291,7 @@ __global__ void k_eoff(int nT, const TileHdr* tiles, const int32_t* ebase, const
   for (int e = T.e0 + threadIdx.x; e < T.e1; e += blockDim.x) {
     int b0 = ebase[3 * (size_t)e], b1 = ebase[3 * (size_t)e + 1], b2 = ebase[3 * (size_t)e + 2];
     uint32_t off = (uint32_t)((b0 - T.ox) + T.pad[0] * (b1 - T.oy) + T.pad[1] * (b2 - T.oz));
-    eoff[e] = off | ((uint32_t)emask_rank(T.emask, ecell[e]) << 16);  // vb slot (compact)
+    eoff[e] = off | ((uint32_t)ecell[e] << 16);  // vb slot = the node's brick cell
     bool ok = true;
     for (int cz = 0; cz < 4 && ok; ++cz)
       for (int cy = 0; cy < 4 && ok; ++cy)

@@ -47,10 +47,9 @@ struct ProfScope {
 void count_launch();
 
 // ------------------------------------------------------------------ band data
-// One tile = one occupied 8^3 brick.  64-bit aligned, 200 bytes.
-// E u of the tile's eval nodes lives in vb[slot * 512 + rank], rank = position of
-// the node's brick cell among the set bits of emask (cell order), so a tile's
-// values are contiguous (compact) and any cell is located by a popcount.
+// One tile = one occupied 8^3 brick.  64-bit aligned, 168 bytes.
+// E u of the tile's eval nodes lives in vb[slot * 512 + cell] (only the cells set
+// in emask are written and read).
 struct TileHdr {
   int32_t e0, e1;      // eval nodes (Sigma_A u Sigma_G in the brick) [e0, e1)
   int32_t a0, a1;      // output (active / owned) nodes [a0, a1)
@@ -61,11 +60,10 @@ struct TileHdr {
   int32_t bx, by, bz;  // brick coordinates (lattice origin = 8*b)
   int32_t pad[3];      // row stride, plane stride of the box; segment id (RAS)
   uint32_t emask[16];  // eval-node cells of the brick (Sigma_A u Sigma_G), bit = cell
-  uint16_t epre[16];   // epre[w] = set bits of emask[0..w)
   int32_t np;          // eval nodes e0 + 2p, e0 + 2p + 1 (p < np) share a stencil base
   int32_t pad2;
 };
-static_assert(sizeof(TileHdr) == 200, "TileHdr layout");
+static_assert(sizeof(TileHdr) == 168, "TileHdr layout");
 
 __host__ __device__ inline int popc32(uint32_t v) {
 #ifdef __CUDA_ARCH__
@@ -73,11 +71,6 @@ __host__ __device__ inline int popc32(uint32_t v) {
 #else
   return __builtin_popcount(v);
 #endif
-}
-__host__ __device__ inline int emask_rank(const uint32_t* m16, int cell) {
-  int w = cell >> 5, r = 0;
-  for (int q = 0; q < w; ++q) r += popc32(m16[q]);
-  return r + popc32(m16[w] & ((1u << (cell & 31)) - 1u));
 }
 
 // A fill run copies len consecutive source doubles u[src..src+len) to
@@ -113,7 +106,7 @@ struct cpm_band {
   double* tx = nullptr;            // nE fractional offsets (SoA)
   double* ty = nullptr;
   double* tz = nullptr;
-  uint32_t* eoff = nullptr;        // nE: box offset (low 16) | vb rank in the tile (high 16)
+  uint32_t* eoff = nullptr;        // nE: box offset (low 16) | brick cell of the node (high 16)
   uint16_t* acell = nullptr;       // nA: brick cell of each output node
   int32_t* aijk = nullptr;         // 3*nA lattice coords (band order)
   int32_t* gijk = nullptr;         // 3*nG lattice coords
