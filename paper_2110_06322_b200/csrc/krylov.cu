@@ -106,24 +106,30 @@ int launch_dcgs_dots(const vec::Seg& S, int k, const double* V, int64_t ldv, con
                      double* partial, int pld, double* out, int ldo, unsigned* counters,
                      cudaStream_t st, const int* skip) {
   const int grid = S.nseg * S.gps;
+  // ring depth: up to 4 stages within ~110 KB (2 blocks per SM)
+  auto depth = [](size_t stage) { return (int)std::max<size_t>(1, std::min<size_t>(4, (110 * 1024) / stage)); };
   if (k <= 64) {
-    const size_t sm = ((size_t)k * (256 + 4) + 256) * sizeof(double);
+    const size_t stage = (size_t)(k + 1) * (256 + 4) * sizeof(double);
+    const int ns = depth(stage);
     static bool attr = false;
     if (!attr) {
       CPM_CUDA(cudaFuncSetAttribute(vec::k_dcgs_dots<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)(((size_t)64 * 260 + 256) * sizeof(double))));
+                                    200 * 1024));
       attr = true;
     }
-    vec::k_dcgs_dots<256><<<grid, 256, sm, st>>>(S, k, V, ldv, z, partial, pld, out, ldo, counters, skip);
+    vec::k_dcgs_dots<256><<<grid, 256, ns * stage, st>>>(S, k, V, ldv, z, partial, pld, out, ldo,
+                                                         counters, skip, ns);
   } else {
+    const size_t stage = (size_t)(k + 1) * (128 + 4) * sizeof(double);
+    const int ns = depth(stage);
     static bool attr = false;
-    const size_t sm2 = ((size_t)k * (128 + 4) + 128) * sizeof(double);
     if (!attr) {
       CPM_CUDA(cudaFuncSetAttribute(vec::k_dcgs_dots<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)(((size_t)(kMaxRestart + 1) * 132 + 128) * sizeof(double))));
+                                    200 * 1024));
       attr = true;
     }
-    vec::k_dcgs_dots<128><<<grid, 128, sm2, st>>>(S, k, V, ldv, z, partial, pld, out, ldo, counters, skip);
+    vec::k_dcgs_dots<128><<<grid, 128, ns * stage, st>>>(S, k, V, ldv, z, partial, pld, out, ldo,
+                                                         counters, skip, ns);
   }
   count_launch();
   CPM_CUDA(cudaGetLastError());

@@ -260,17 +260,28 @@ static __global__ void __launch_bounds__(TB) k_proj(Seg S, int k, const double* 
 //                  V_{j+1} <- (z - mu u_j - sum_i e_i Q_i) / rho
 //   (b = coef[0..j), e = coef[ldc .. ldc + j), rho = coef[2 ldc], mu = coef[2 ldc + 1];
 //   segment s reads coef + s * cstride)
+__device__ __forceinline__ void cp_wait_pending(int n) {  // all but the newest n groups
+  switch (n) {
+    case 0: asm volatile("cp.async.wait_group 0;\n" ::: "memory"); break;
+    case 1: asm volatile("cp.async.wait_group 1;\n" ::: "memory"); break;
+    case 2: asm volatile("cp.async.wait_group 2;\n" ::: "memory"); break;
+    default: asm volatile("cp.async.wait_group 3;\n" ::: "memory"); break;
+  }
+}
+
+// Tiles are staged through a ring of ns stages (ns = 1..4, chosen by the launcher
+// from k): the copies of the next ns - 1 tiles are in flight while a tile's
+// column dots run.  Per thread the tiles and elements are summed in the same
+// order for every ns.
 template <int TB>
 static __global__ void __launch_bounds__(TB) k_dcgs_dots(Seg S, int k, const double* __restrict__ V,
                                                          int64_t ldv, const double* __restrict__ z,
                                                          double* partial, int pld, double* out,
                                                          int ldo, unsigned* counters,
-                                                         const int* __restrict__ skip) {
+                                                         const int* __restrict__ skip, int ns) {
   if (skip && *skip) return;
   constexpr int SV = TB + 4;
-  extern __shared__ double smp[];
-  double* sv = smp;             // k columns of SV
-  double* sz = sv + (size_t)k * SV;
+  extern __shared__ double smp[];  // ns stages of k + 1 columns (Q_0 .. Q_{j-1}, u_j, z)
   __shared__ bool last;
   const int s = blockIdx.x / S.gps, lb = blockIdx.x % S.gps;
   const int64_t o0 = S.off[s], n = S.off[s + 1] - o0;
@@ -279,24 +290,32 @@ static __global__ void __launch_bounds__(TB) k_dcgs_dots(Seg S, int k, const dou
   while (kp < k) kp <<= 1;
   const int P = kp >= TB ? 1 : TB / kp;
   const int col = tid / P, sub = tid % P;
-  const double* su = sv + (size_t)(k - 1) * SV;  // the lagged vector is the last column
-  double a1 = 0.0, a2 = 0.0;
-  for (int64_t t0 = (int64_t)lb * TB; t0 < n; t0 += (int64_t)S.gps * TB) {
+  const size_t stage = (size_t)(k + 1) * SV;
+  const int64_t stride = (int64_t)S.gps * TB;
+  auto issue = [&](int64_t t0, double* buf) {
     const int64_t e = t0 + tid;
-    const bool in = e < n;
-    if (in) {
+    if (e < n) {
       const double* p = V + o0 + e;
-      for (int i = 0; i < k; ++i) cpa8(sv + (size_t)i * SV + tid, p + (size_t)i * ldv);
+      for (int i = 0; i < k; ++i) cpa8(buf + (size_t)i * SV + tid, p + (size_t)i * ldv);
+      cpa8(buf + (size_t)k * SV + tid, z + o0 + e);
+    } else if (t0 < n) {
+      for (int i = 0; i <= k; ++i) buf[(size_t)i * SV + tid] = 0.0;
     }
-    cp_commit_v();
-    const double zv = in ? z[o0 + e] : 0.0;
-    cp_wait_all_v();
-    if (!in)
-      for (int i = 0; i < k; ++i) sv[(size_t)i * SV + tid] = 0.0;
-    sz[tid] = zv;
+    cp_commit_v();  // one group per tile, possibly empty
+  };
+  const int64_t tfirst = (int64_t)lb * TB;
+  for (int q = 0; q < ns - 1; ++q) issue(tfirst + q * stride, smp + (size_t)q * stage);
+  double a1 = 0.0, a2 = 0.0;
+  int it = 0;
+  for (int64_t t0 = tfirst; t0 < n; t0 += stride, ++it) {
+    issue(t0 + (int64_t)(ns - 1) * stride, smp + (size_t)((it + ns - 1) % ns) * stage);
+    cp_wait_pending(ns - 1);
     __syncthreads();
+    const double* sv = smp + (size_t)(it % ns) * stage;
     if (col < k) {
       const double* c = sv + (size_t)col * SV;
+      const double* su = sv + (size_t)(k - 1) * SV;  // the lagged vector is the last column
+      const double* sz = sv + (size_t)k * SV;
       for (int q = sub; q < TB; q += P) {
         const double cv = c[q];
         a1 += cv * su[q];
@@ -305,6 +324,7 @@ static __global__ void __launch_bounds__(TB) k_dcgs_dots(Seg S, int k, const dou
     }
     __syncthreads();
   }
+  cp_wait_all_v();
   for (int o = P >> 1; o > 0; o >>= 1) {
     a1 += __shfl_xor_sync(0xffffffffu, a1, o);
     a2 += __shfl_xor_sync(0xffffffffu, a2, o);
