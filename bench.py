@@ -8,6 +8,8 @@ unit sphere, h = 1/200 (~4.1M band nodes), fp64:
 `value` = band-node applies per second over the timed applies (CUDA events on the
 launching stream, max over ranks); `solve` reports the GMRES solve time.  The
 band is built once, outside the timed region (its build time is reported).
+Outside the timed steps, rank 0 also reports `config4_rd` (config-4 IMEX steps)
+and `config2_solve` (one config-2 RAS-FGMRES solve, ~40 s; --c2-kinner 0 skips it).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
 
@@ -316,6 +318,31 @@ def run_mine(args):
         except Exception as e:  # report, never fail the main metric
             rd = {"error": str(e)[:200]}
 
+    # config 2 (torus h = 1/400, RAS-FGMRES(50), 8 subdomains, overlap 4h): one solve, 1 GPU
+    c2 = None
+    if args.c2_kinner > 0 and rank == 0:
+        try:
+            cb = cpm.cpm_build_band("torus", 1.0 / 400, R=1.0, r=0.4)
+            cf = torch.empty(cb.n, dtype=torch.float64, device=dev)
+            cpm.cpm_eval_torus_rhs(cb, seeded_inputs.smooth_modulation_coeffs(1), cf)
+            cras = cpm.cpm_ras_setup(cb, 8, 4, args.c2_kinner, 1.0)
+            cu = torch.zeros_like(cf)
+            ca = torch.cuda.Event(enable_timing=True)
+            cbv = torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            ca.record(stream)
+            cst = cpm.cpm_solve(cb, 1.0, cf, cu, rtol=1e-10, restart=50, ras=cras)
+            cbv.record(stream)
+            torch.cuda.synchronize()
+            c2 = {"workload": "BASELINE configs[2]: torus R=1 r=0.4, h=1/400, c=1, f=cos(3theta)sin(2phi)"
+                              "(1 + seed-1 smooth modulation); RAS-FGMRES(50), 8 Morton-slab subdomains, "
+                              f"overlap 4h, {args.c2_kinner} inner GMRES steps, rtol 1e-10, 1 GPU",
+                  "n_active": cb.n, "solve_s": ca.elapsed_time(cbv) / 1e3, "iterations": cst.iterations,
+                  "converged": bool(cst.converged), "resid_true_rel": cst.resid_true / cst.bnorm}
+            del cras, cb, cf, cu
+        except Exception as e:  # report, never fail the main metric
+            c2 = {"error": str(e)[:200]}
+
     # e2e: same metric through the C ABI with HOST buffers (pinned), copies inside the timed region
     y_host = torch.empty(nA, dtype=torch.float64).pin_memory()
     u_np, y_np = u_host.numpy(), y_host.numpy()
@@ -396,6 +423,7 @@ def run_mine(args):
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 8 * nA * CFG["applies"],
                     "d2h_bytes_per_step": 8 * nA * CFG["applies"]},
             "config4_rd": rd,
+            "config2_solve": c2,
             "gpu_launches": launches,
             "clocks": clk,
         }
@@ -415,6 +443,8 @@ def main():
     ap.add_argument("--ref-rows", type=int, default=1 << 16)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--rd-steps", type=int, default=20, help="config-4 IMEX steps timed (0: skip)")
+    ap.add_argument("--c2-kinner", type=int, default=16,
+                    help="inner GMRES steps of the config-2 RAS solve (0: skip that solve)")
     args = ap.parse_args()
     if args.warmup < 3:
         print("warning: --warmup < 3 violates the timing rules; using 3", file=sys.stderr)
