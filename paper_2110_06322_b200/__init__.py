@@ -10,6 +10,7 @@ from .cpm import (  # noqa: F401
     CpmError,
     cpm_apply,
     cpm_band_active_coords,
+    cpm_band_eval_order,
     cpm_band_ghost_coords,
     cpm_build_band,
     cpm_eval_sph,

@@ -79,6 +79,7 @@ _SIGS = {
     "cpm_band_get_info": (ctypes.c_int, [_vp, ctypes.POINTER(_BandInfo)]),
     "cpm_band_active_coords": (ctypes.c_int, [_vp, _vp]),
     "cpm_band_ghost_coords": (ctypes.c_int, [_vp, _vp]),
+    "cpm_band_eval_order": (ctypes.c_int, [_vp, _vp, _vp]),
     "cpm_band_free": (None, [_vp]),
     "cpm_apply": (ctypes.c_int, [_vp, ctypes.c_double, _vp, _vp, _vp]),
     "cpm_solve": (ctypes.c_int, [_vp, ctypes.c_double, _vp, _vp, ctypes.c_double, ctypes.c_int,
@@ -248,6 +249,18 @@ def cpm_band_ghost_coords(band: Band) -> np.ndarray:
     out = np.empty((band.info.n_ghost, 3), dtype=np.int32)
     _check(load_library().cpm_band_ghost_coords(band.handle, out.ctypes.data), "cpm_band_ghost_coords")
     return out
+
+
+def cpm_band_eval_order(band: Band):
+    """(tiles[n_tiles, 6] = e0, e1, np, row stride, plane stride, box cells; eoff[e1 of the
+    last tile]) — diagnostics of the extend's node order (include/cpm.h)."""
+    lib = load_library()
+    tiles = np.empty((band.info.n_tiles, 6), dtype=np.int32)
+    _check(lib.cpm_band_eval_order(band.handle, tiles.ctypes.data, None), "cpm_band_eval_order")
+    ne = int(tiles[-1, 1]) if len(tiles) else 0
+    eoff = np.empty(ne, dtype=np.uint32)
+    _check(lib.cpm_band_eval_order(band.handle, tiles.ctypes.data, eoff.ctypes.data), "cpm_band_eval_order")
+    return tiles, eoff
 
 
 def cpm_apply(band: Band, c: float, u, y, stream=None):

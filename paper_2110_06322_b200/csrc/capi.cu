@@ -162,6 +162,27 @@ int cpm_band_ghost_coords(const cpm_band* b, int32_t* ijk_host) {
   return CPM_OK;
 }
 
+int cpm_band_eval_order(const cpm_band* b, int32_t* tiles_host, uint32_t* eoff_host) {
+  if (!b || !tiles_host) return fail(CPM_ERR_ARG, "cpm_band_eval_order: null argument");
+  std::vector<TileHdr> T((size_t)b->nT);
+  if (b->nT > 0)
+    CPM_CUDA(cudaMemcpy(T.data(), b->tiles, sizeof(TileHdr) * b->nT, cudaMemcpyDeviceToHost));
+  for (int64_t t = 0; t < b->nT; ++t) {
+    int32_t* o = tiles_host + 6 * t;
+    o[0] = T[t].e0;
+    o[1] = T[t].e1;
+    o[2] = T[t].np;
+    o[3] = T[t].pad[0];
+    o[4] = T[t].pad[1];
+    o[5] = T[t].pad[1] * T[t].sz;
+  }
+  if (eoff_host && b->nT > 0) {
+    const int64_t ne = T[b->nT - 1].e1;
+    CPM_CUDA(cudaMemcpy(eoff_host, b->eoff, sizeof(uint32_t) * ne, cudaMemcpyDeviceToHost));
+  }
+  return CPM_OK;
+}
+
 void cpm_band_free(cpm_band* b) { free_band(b); }
 
 int cpm_apply(const cpm_band* b, double c, const double* u, double* y, void* stream) {
