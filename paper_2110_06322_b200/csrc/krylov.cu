@@ -109,7 +109,7 @@ int launch_dcgs_dots(const vec::Seg& S, int k, const double* V, int64_t ldv, con
   // ring depth: up to 4 stages within ~110 KB (2 blocks per SM)
   auto depth = [](size_t stage) { return (int)std::max<size_t>(1, std::min<size_t>(4, (110 * 1024) / stage)); };
   if (k <= 64) {
-    const size_t stage = (size_t)(k + 1) * (256 + 4) * sizeof(double);
+    const size_t stage = (size_t)(k + 1) * (256 + 2 * vec::dots_threads_per_col(256, k)) * sizeof(double);
     const int ns = depth(stage);
     static bool attr = false;
     if (!attr) {
@@ -120,7 +120,7 @@ int launch_dcgs_dots(const vec::Seg& S, int k, const double* V, int64_t ldv, con
     vec::k_dcgs_dots<256><<<grid, 256, ns * stage, st>>>(S, k, V, ldv, z, partial, pld, out, ldo,
                                                          counters, skip, ns);
   } else {
-    const size_t stage = (size_t)(k + 1) * (128 + 4) * sizeof(double);
+    const size_t stage = (size_t)(k + 1) * (128 + 2 * vec::dots_threads_per_col(128, k)) * sizeof(double);
     const int ns = depth(stage);
     static bool attr = false;
     if (!attr) {

@@ -269,10 +269,20 @@ __device__ __forceinline__ void cp_wait_pending(int n) {  // all but the newest 
   }
 }
 
+// Threads per column P and the stage layout of k_dcgs_dots: element e of a tile
+// column sits at (e % P) * R + e / P, R = TB / P + 2, so the elements one thread
+// sums (e = sub, sub + P, ...) are adjacent (16-byte loads) and the cp.async
+// writes of a warp spread over the banks; a column takes P * R = TB + 2P doubles.
+__host__ __device__ inline int dots_threads_per_col(int TB, int k) {
+  int kp = 8;
+  while (kp < k) kp <<= 1;
+  return kp >= TB ? 1 : TB / kp;
+}
+
 // Tiles are staged through a ring of ns stages (ns = 1..4, chosen by the launcher
 // from k): the copies of the next ns - 1 tiles are in flight while a tile's
 // column dots run.  Per thread the tiles and elements are summed in the same
-// order for every ns.
+// order for every ns and layout.
 template <int TB>
 static __global__ void __launch_bounds__(TB) k_dcgs_dots(Seg S, int k, const double* __restrict__ V,
                                                          int64_t ldv, const double* __restrict__ z,
@@ -280,26 +290,25 @@ static __global__ void __launch_bounds__(TB) k_dcgs_dots(Seg S, int k, const dou
                                                          int ldo, unsigned* counters,
                                                          const int* __restrict__ skip, int ns) {
   if (skip && *skip) return;
-  constexpr int SV = TB + 4;
   extern __shared__ double smp[];  // ns stages of k + 1 columns (Q_0 .. Q_{j-1}, u_j, z)
   __shared__ bool last;
   const int s = blockIdx.x / S.gps, lb = blockIdx.x % S.gps;
   const int64_t o0 = S.off[s], n = S.off[s + 1] - o0;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  int kp = 8;
-  while (kp < k) kp <<= 1;
-  const int P = kp >= TB ? 1 : TB / kp;
+  const int P = dots_threads_per_col(TB, k);
+  const int M = TB / P, R = M + 2, SV = TB + 2 * P;
   const int col = tid / P, sub = tid % P;
+  const int pos = (tid % P) * R + tid / P;  // where this thread's element is staged
   const size_t stage = (size_t)(k + 1) * SV;
   const int64_t stride = (int64_t)S.gps * TB;
   auto issue = [&](int64_t t0, double* buf) {
     const int64_t e = t0 + tid;
     if (e < n) {
       const double* p = V + o0 + e;
-      for (int i = 0; i < k; ++i) cpa8(buf + (size_t)i * SV + tid, p + (size_t)i * ldv);
-      cpa8(buf + (size_t)k * SV + tid, z + o0 + e);
+      for (int i = 0; i < k; ++i) cpa8(buf + (size_t)i * SV + pos, p + (size_t)i * ldv);
+      cpa8(buf + (size_t)k * SV + pos, z + o0 + e);
     } else if (t0 < n) {
-      for (int i = 0; i <= k; ++i) buf[(size_t)i * SV + tid] = 0.0;
+      for (int i = 0; i <= k; ++i) buf[(size_t)i * SV + pos] = 0.0;
     }
     cp_commit_v();  // one group per tile, possibly empty
   };
@@ -313,13 +322,15 @@ static __global__ void __launch_bounds__(TB) k_dcgs_dots(Seg S, int k, const dou
     __syncthreads();
     const double* sv = smp + (size_t)(it % ns) * stage;
     if (col < k) {
-      const double* c = sv + (size_t)col * SV;
-      const double* su = sv + (size_t)(k - 1) * SV;  // the lagged vector is the last column
-      const double* sz = sv + (size_t)k * SV;
-      for (int q = sub; q < TB; q += P) {
-        const double cv = c[q];
-        a1 += cv * su[q];
-        a2 += cv * sz[q];
+      const double2* c = (const double2*)(sv + (size_t)col * SV + sub * R);
+      const double2* su = (const double2*)(sv + (size_t)(k - 1) * SV + sub * R);  // lagged u_j
+      const double2* sz = (const double2*)(sv + (size_t)k * SV + sub * R);
+      for (int m = 0; m < M / 2; ++m) {  // elements sub + P (2m), sub + P (2m + 1)
+        const double2 cv = c[m], uv = su[m], zv = sz[m];
+        a1 += cv.x * uv.x;
+        a2 += cv.x * zv.x;
+        a1 += cv.y * uv.y;
+        a2 += cv.y * zv.y;
       }
     }
     __syncthreads();
