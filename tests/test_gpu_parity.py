@@ -115,6 +115,44 @@ def test_apply_parity(cpm, kind, h, kw, c):
     assert err <= APPLY_TOL, err
 
 
+@pytest.mark.parametrize("kind,h,kw", [CASES[0], CASES[2], CASES[4]])
+def test_outputs_written_only_in_range(cpm, kind, h, kw):
+    """Sentinels around the caller's vectors: apply, solve and RAS apply write
+    exactly their n outputs (every one of them) and nothing before or after."""
+    gb = _gpu_band(cpm, kind, h, **kw)
+    n, pad = gb.n, 4096
+    ga = cpm.cpm_band_active_coords(gb).astype(np.int64)
+    u = torch.from_numpy(seeded_inputs.uniform_pm1(0, ga)).cuda()
+    sentinel = 12345.0
+
+    def guarded():
+        buf = torch.full((n + 2 * pad,), sentinel, dtype=torch.float64, device="cuda")
+        return buf, buf[pad:pad + n]
+
+    def intact(buf):
+        torch.cuda.synchronize()
+        return bool((buf[:pad] == sentinel).all()) and bool((buf[pad + n:] == sentinel).all())
+
+    yb, y = guarded()
+    cpm.cpm_apply(gb, 1.0, u, y)
+    assert intact(yb) and not bool((y == sentinel).any())
+    # inputs inside NaN padding: a read outside [0, n) would show up in the result
+    ub = torch.full((n + 2 * pad,), float("nan"), dtype=torch.float64, device="cuda")
+    ub[pad:pad + n] = u
+    y2 = torch.empty_like(u)
+    cpm.cpm_apply(gb, 1.0, ub[pad:pad + n], y2)
+    torch.cuda.synchronize()
+    assert torch.equal(y2, y)
+    xb, x = guarded()
+    x.zero_()
+    st = cpm.cpm_solve(gb, 1.0, u, x, rtol=1e-6, restart=20, maxit=60)
+    assert intact(xb) and st.iterations > 0
+    ras = cpm.cpm_ras_setup(gb, 4, 2, 4, 1.0)
+    zb, z = guarded()
+    cpm.cpm_ras_apply(ras, u, z)
+    assert intact(zb) and not bool((z == sentinel).any())
+
+
 def test_apply_host_pointers_match_device(cpm):
     gb = _gpu_band(cpm, "sphere", 0.1)
     ga = cpm.cpm_band_active_coords(gb).astype(np.int64)
