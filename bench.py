@@ -407,7 +407,8 @@ def run_mine(args):
                          "alg_bytes_per_apply": alg_bytes,
                          "apply_ms": mean_apply_s * 1e3,
                          "extend_ms": ext_ms / max(ext_n, 1), "laplace_ms": lap_ms / max(lap_n, 1),
-                         "note": "extend is bound by shared-memory gathers (DESIGN.md §Kernels); "
+                         "note": "extend is bound by its per-tile load chain overlapped with FP64 and "
+                                 "shared-memory gathers (DESIGN.md §Kernels, ablations); "
                                  "traffic = ncu DRAM bytes per apply (profiles/r01_traffic.json)"},
             "roofline_solve": {"kernel": "Krylov passes of the solve (k_dcgs_dots + k_dcgs_update), "
                                          "the largest share of a step",
