@@ -5,7 +5,7 @@
  * "A closest point method library for PDEs on surfaces with parallel domain
  * decomposition solvers and preconditioners" (arXiv:2110.06322), reproduced in
  * PAPER.md; "PAPER.md:N" below cites its line N.  DESIGN.md lists the readings
- * (R1..R14) taken where the paper is silent.
+ * (R1..R15) taken where the paper is silent.
  *
  * Conventions (all entry points):
  *  - Return CPM_OK (0) on success, a negative CPM_ERR_* code otherwise; the
@@ -129,7 +129,8 @@ int cpm_apply(const cpm_band* band, double c, const double* u, double* y, void* 
 /* ---------------------------------------------------------------- Krylov solve
  * cpm_solve — solve (c - Delta_S^h) u = f (Eq. 2) by restarted GMRES(restart)
  * (GMRES is the default solver) with classical Gram-Schmidt
- * applied twice (CGS2), fused dot/axpy/norm kernels, deterministic reductions.
+ * applied twice (CGS2; without ras in its delayed one-reduction form DCGS2,
+ * reading R15), fused dot/axpy/norm kernels, deterministic reductions.
  * Right-preconditioned flexible GMRES when `ras` is not NULL.
  * Convention (reading R5): u holds the initial guess on entry (pass zeros for
  * x0 = 0) and the solution on exit; convergence when the Givens residual
