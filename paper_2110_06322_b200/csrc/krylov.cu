@@ -102,9 +102,10 @@ const bool g_force_cgs2 = [] {
 }();
 }  // namespace
 
-int launch_dcgs_dots(const vec::Seg& S, int k, const double* V, int64_t ldv, const double* z,
-                     double* partial, int pld, double* out, int ldo, unsigned* counters,
-                     cudaStream_t st, const int* skip) {
+template <class Epi>
+static int launch_dcgs_dots_epi(const vec::Seg& S, int k, const double* V, int64_t ldv, const double* z,
+                                double* partial, int pld, double* out, int ldo, unsigned* counters,
+                                cudaStream_t st, const int* skip, Epi epi) {
   const int grid = S.nseg * S.gps;
   // ring depth: up to 4 stages within ~110 KB (2 blocks per SM)
   auto depth = [](size_t stage) { return (int)std::max<size_t>(1, std::min<size_t>(4, (110 * 1024) / stage)); };
@@ -113,27 +114,33 @@ int launch_dcgs_dots(const vec::Seg& S, int k, const double* V, int64_t ldv, con
     const int ns = depth(stage);
     static bool attr = false;
     if (!attr) {
-      CPM_CUDA(cudaFuncSetAttribute(vec::k_dcgs_dots<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      CPM_CUDA(cudaFuncSetAttribute(vec::k_dcgs_dots<256, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     200 * 1024));
       attr = true;
     }
-    vec::k_dcgs_dots<256><<<grid, 256, ns * stage, st>>>(S, k, V, ldv, z, partial, pld, out, ldo,
-                                                         counters, skip, ns);
+    vec::k_dcgs_dots<256, Epi><<<grid, 256, ns * stage, st>>>(S, k, V, ldv, z, partial, pld, out, ldo,
+                                                              counters, skip, ns, epi);
   } else {
     const size_t stage = (size_t)(k + 1) * (128 + 2 * vec::dots_threads_per_col(128, k)) * sizeof(double);
     const int ns = depth(stage);
     static bool attr = false;
     if (!attr) {
-      CPM_CUDA(cudaFuncSetAttribute(vec::k_dcgs_dots<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      CPM_CUDA(cudaFuncSetAttribute(vec::k_dcgs_dots<128, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     200 * 1024));
       attr = true;
     }
-    vec::k_dcgs_dots<128><<<grid, 128, ns * stage, st>>>(S, k, V, ldv, z, partial, pld, out, ldo,
-                                                         counters, skip, ns);
+    vec::k_dcgs_dots<128, Epi><<<grid, 128, ns * stage, st>>>(S, k, V, ldv, z, partial, pld, out, ldo,
+                                                              counters, skip, ns, epi);
   }
   count_launch();
   CPM_CUDA(cudaGetLastError());
   return CPM_OK;
+}
+
+int launch_dcgs_dots(const vec::Seg& S, int k, const double* V, int64_t ldv, const double* z,
+                     double* partial, int pld, double* out, int ldo, unsigned* counters,
+                     cudaStream_t st, const int* skip) {
+  return launch_dcgs_dots_epi(S, k, V, ldv, z, partial, pld, out, ldo, counters, st, skip, vec::NoEpi());
 }
 
 int launch_dcgs_update(const vec::Seg& S, int k, double* V, int64_t ldv, const double* z,
@@ -222,15 +229,18 @@ __global__ void k_arnoldi_step(GState* st, int j, int m) {
 // and the next lagged vector u_{j+1} = (z - mu u_j - Q (d - mu b))/rho
 // (k_dcgs_update, coefficients in st->coef).
 constexpr int kStepThreads = 128;
-__global__ void __launch_bounds__(kStepThreads) k_dcgs_step(GState* st, int j, int m, int maxit) {
+// Run by one block of nt = blockDim.x threads (<= 256): the k_dcgs_step kernel, or
+// the block of k_dcgs_dots that finishes the reduction (single-GPU solves, where
+// no allreduce sits between the two).
+__device__ void dcgs_step_body(GState* st, int j, int m, int maxit) {
   if (st->done) return;  // a step queued past convergence
-  const int ld = kMaxRestart + 1, k = j + 1, tid = threadIdx.x;
+  const int ld = kMaxRestart + 1, k = j + 1, tid = threadIdx.x, nt = blockDim.x;
   const double* b = st->red;
   const double* d = st->red + k;
-  __shared__ double sbb[kStepThreads / 32], sbd[kStepThreads / 32];
+  __shared__ double sbb[8], sbd[8];
   __shared__ int sdone;
   double pbb = 0.0, pbd = 0.0;
-  for (int i = tid; i < j; i += kStepThreads) {
+  for (int i = tid; i < j; i += nt) {
     pbb += b[i] * b[i];
     pbd += b[i] * d[i];
   }
@@ -242,7 +252,7 @@ __global__ void __launch_bounds__(kStepThreads) k_dcgs_step(GState* st, int j, i
   }
   __syncthreads();
   double bb = 0.0, bd = 0.0;
-  for (int w = 0; w < kStepThreads / 32; ++w) {
+  for (int w = 0; w < nt / 32; ++w) {
     bb += sbb[w];
     bd += sbd[w];
   }
@@ -251,7 +261,7 @@ __global__ void __launch_bounds__(kStepThreads) k_dcgs_step(GState* st, int j, i
   const int brk = !(rho2 > 1e-28 * alpha);
   const double rho = brk ? 0.0 : sqrt(rho2);
   if (j >= 1)
-    for (int i = tid; i < j; i += kStepThreads) st->Hr[(size_t)(j - 1) * ld + i] = st->cpend[i] + b[i];
+    for (int i = tid; i < j; i += nt) st->Hr[(size_t)(j - 1) * ld + i] = st->cpend[i] + b[i];
   __syncthreads();
   if (tid == 0) {
     sdone = 0;
@@ -295,13 +305,13 @@ __global__ void __launch_bounds__(kStepThreads) k_dcgs_step(GState* st, int j, i
   const double mu = (gamma - bd) / rho2;
   double* cb = st->coef;
   double* ce = st->coef + (kMaxRestart + 2);
-  for (int l = tid; l <= j; l += kStepThreads) {
+  for (int l = tid; l <= j; l += nt) {
     double gl = 0.0;  // (Hr b)_l, Hr[l, i] = 0 for l > i + 1
     for (int i = (l > 0 ? l - 1 : 0); i < j; ++i) gl += st->Hr[(size_t)i * ld + l] * b[i];
     const double ql = l < j ? d[l] : rho * mu;
     st->cpend[l] = (ql - gl) / rho;
   }
-  for (int i = tid; i < j; i += kStepThreads) {
+  for (int i = tid; i < j; i += nt) {
     cb[i] = b[i];
     ce[i] = d[i] - mu * b[i];
   }
@@ -310,6 +320,14 @@ __global__ void __launch_bounds__(kStepThreads) k_dcgs_step(GState* st, int j, i
     st->coef[2 * (kMaxRestart + 2) + 1] = mu;
   }
 }
+__global__ void __launch_bounds__(kStepThreads) k_dcgs_step(GState* st, int j, int m, int maxit) {
+  dcgs_step_body(st, j, m, maxit);
+}
+struct StepEpi {
+  GState* st;
+  int j, m, maxit;
+  __device__ void operator()(int) const { dcgs_step_body(st, j, m, maxit); }
+};
 
 // Back substitution H(0:k,0:k) y = g(0:k), one warp (lanes split the row sums).
 __global__ void k_lsq(GState* st) {
@@ -458,13 +476,17 @@ int gmres_device(const LinOp& A, const PrecOp* M, const double* b, double* x, in
         double* Vj = ws.V + (size_t)j * ws.ldv;
         if (j < m) CPM_TRY(A.apply(Vj, ws.w, nullptr, skip, s));  // z = A u_j
         const int k = j + 1;
-        {
+        if (!A.allreduce) {  // one GPU: the reducing block runs the step (no extra launch)
           ProfScope ps(K_MDOT, s);
-          CPM_TRY(launch_dcgs_dots(S, k, ws.V, ws.ldv, ws.w, ws.partial, 2 * kLdc + 8, st->red, 0, cnt + 1,
-                                   s, skip));
-          CPM_TRY(allreduce(st->red, 2 * k));
-        }
-        {
+          CPM_TRY(launch_dcgs_dots_epi(S, k, ws.V, ws.ldv, ws.w, ws.partial, 2 * kLdc + 8, st->red, 0,
+                                       cnt + 1, s, skip, StepEpi{st, j, m, maxit}));
+        } else {
+          {
+            ProfScope ps(K_MDOT, s);
+            CPM_TRY(launch_dcgs_dots(S, k, ws.V, ws.ldv, ws.w, ws.partial, 2 * kLdc + 8, st->red, 0,
+                                     cnt + 1, s, skip));
+            CPM_TRY(allreduce(st->red, 2 * k));
+          }
           ProfScope ps(K_OTHER, s);
           k_dcgs_step<<<1, kStepThreads, 0, s>>>(st, j, m, maxit);
           count_launch();

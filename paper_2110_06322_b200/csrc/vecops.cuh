@@ -283,12 +283,18 @@ __host__ __device__ inline int dots_threads_per_col(int TB, int k) {
 // from k): the copies of the next ns - 1 tiles are in flight while a tile's
 // column dots run.  Per thread the tiles and elements are summed in the same
 // order for every ns and layout.
-template <int TB>
+struct NoEpi {
+  __device__ void operator()(int) const {}
+};
+// Epi: run by every thread of the block that finishes the reduction of segment s,
+// after out[s * ldo + 0 .. 2k) is written (e.g. the GMRES step that consumes it).
+template <int TB, class Epi = NoEpi>
 static __global__ void __launch_bounds__(TB) k_dcgs_dots(Seg S, int k, const double* __restrict__ V,
                                                          int64_t ldv, const double* __restrict__ z,
                                                          double* partial, int pld, double* out,
                                                          int ldo, unsigned* counters,
-                                                         const int* __restrict__ skip, int ns) {
+                                                         const int* __restrict__ skip, int ns,
+                                                         Epi epi = Epi()) {
   if (skip && *skip) return;
   extern __shared__ double smp[];  // ns stages of k + 1 columns (Q_0 .. Q_{j-1}, u_j, z)
   __shared__ bool last;
@@ -355,6 +361,8 @@ static __global__ void __launch_bounds__(TB) k_dcgs_dots(Seg S, int k, const dou
     if (lane == 0) out[(size_t)s * ldo + i] = a;
   }
   if (tid == 0) counters[s] = 0u;
+  __syncthreads();  // out[] written by this block is visible to all its threads
+  epi(s);
 }
 
 template <int TB>
