@@ -260,6 +260,16 @@ static __global__ void __launch_bounds__(TB) k_proj(Seg S, int k, const double* 
 //                  V_{j+1} <- (z - mu u_j - sum_i e_i Q_i) / rho
 //   (b = coef[0..j), e = coef[ldc .. ldc + j), rho = coef[2 ldc], mu = coef[2 ldc + 1];
 //   segment s reads coef + s * cstride)
+// L2 prefetch of [p, p + n) doubles (bulk, 16-byte granules; the vectors are
+// allocated with a stride padded to 64 doubles, so rounding stays inside them).
+__device__ __forceinline__ void prefetch_l2(const double* p, int64_t n) {
+  if (n <= 0) return;
+  const uintptr_t a0 = (uintptr_t)p & ~(uintptr_t)15;
+  const uintptr_t a1 = ((uintptr_t)(p + n) + 15) & ~(uintptr_t)15;
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(a0), "r"((unsigned)(a1 - a0))
+               : "memory");
+}
+
 __device__ __forceinline__ void cp_wait_pending(int n) {  // all but the newest n groups
   switch (n) {
     case 0: asm volatile("cp.async.wait_group 0;\n" ::: "memory"); break;
@@ -324,6 +334,10 @@ static __global__ void __launch_bounds__(TB) k_dcgs_dots(Seg S, int k, const dou
   int it = 0;
   for (int64_t t0 = tfirst; t0 < n; t0 += stride, ++it) {
     issue(t0 + (int64_t)(ns - 1) * stride, smp + (size_t)((it + ns - 1) % ns) * stage);
+    {  // the tile after the ring window: into L2 while this one is reduced
+      const int64_t tp = t0 + (int64_t)ns * stride;  // (1 or 2 tiles further: slower)
+      if (tid <= k && tp < n) prefetch_l2((tid < k ? V + (size_t)tid * ldv : z) + o0 + tp, min((int64_t)TB, n - tp));
+    }
     cp_wait_pending(ns - 1);
     __syncthreads();
     const double* sv = smp + (size_t)(it % ns) * stage;
