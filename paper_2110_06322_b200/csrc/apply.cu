@@ -10,16 +10,19 @@
 //             8 lanes per run, cp.async); for every eval node (Sigma_A u Sigma_G in
 //             the brick) recompute the tricubic Lagrange weights from its fractional
 //             offsets and contract x, then y, then z.  A tile's nodes
-//             are ordered (build time) so the 16 lanes of a half-warp read distinct
-//             banks or the same address (broadcast).  E u goes to the tile's compact
-//             slot range of vb (cell order, TileHdr::emask ranks).
+//             are ordered (build time) so adjacent lane pairs read one address and
+//             the 16 pair addresses of a warp distinct banks.  E u goes to
+//             vb[tile * 512 + cell].
 //   k_laplace (one CTA of 128 threads per tile): gather the tile's E u and the face
 //             layers of its 6 neighbour tiles into a dense 10^3 halo brick in shared
 //             memory, then the 7-point combination for every output node.
+// Both kernels bulk-prefetch into L2 the per-tile data of the tile a CTA one
+// residency wave later will take, so its dependent loads hit L2.
 // No tensor cores: this is a gather, not a dense contraction.  The extend is
-// bound by shared-memory wavefronts (64 8-byte gathers per node) and FP64 issue,
-// the laplace by load latency; DESIGN.md §Kernels has the measured rooflines.
+// bound by its per-tile load chain overlapped with FP64 issue and shared-memory
+// gathers, the laplace by load latency; DESIGN.md §Kernels has the measurements.
 #include <algorithm>
+#include <cstdlib>
 
 #include "internal.cuh"
 
@@ -87,6 +90,15 @@ __device__ __forceinline__ uint32_t ld_hint(const uint32_t* p, uint64_t pol) {
                : "l"(p), "l"(pol));
   return v;
 }
+// L2 prefetch of [p, p + bytes), widened to 16-byte granules (the arrays are
+// allocated with padding, so the rounding stays inside them).
+__device__ __forceinline__ void prefetch_l2_bytes(const void* p, size_t bytes) {
+  if (bytes == 0) return;
+  const uintptr_t a0 = (uintptr_t)p & ~(uintptr_t)15;
+  const uintptr_t a1 = ((uintptr_t)p + bytes + 15) & ~(uintptr_t)15;
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(a0), "r"((unsigned)(a1 - a0))
+               : "memory");
+}
 __device__ __forceinline__ void st_hint(double* p, double v, uint64_t pol) {
   asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;\n" ::"l"(p), "d"(v), "l"(pol) : "memory");
 }
@@ -134,7 +146,7 @@ __global__ void __launch_bounds__(kNtThreads, 8)
                 const double* __restrict__ uh, uint32_t split, const double* __restrict__ tx,
                 const double* __restrict__ ty, const double* __restrict__ tz,
                 const uint32_t* __restrict__ eoff, double* __restrict__ vb,
-                const int* __restrict__ skip) {
+                const int* __restrict__ skip, int pfd) {
   if (skip && *skip) return;
   extern __shared__ double smn[];
   double* box = smn;
@@ -183,6 +195,18 @@ __global__ void __launch_bounds__(kNtThreads, 8)
     }
     cp_commit();
   }
+  // The tile a CTA about one residency wave later will take (t + pfd): its
+  // descriptors and node offsets into L2 now, so that CTA's dependent loads are
+  // L2 hits (one lane; the header load it needs is itself that CTA's first load).
+  if (tid == kNtThreads - 32 && t + pfd < (int)gridDim.x) {
+    const TileHdr* F = tiles + t + pfd;
+    const int f0 = F->e0, f1 = F->e1, q0 = F->r0, q1 = F->r1;
+    prefetch_l2_bytes(runs + q0, (size_t)(q1 - q0) * 8);
+    prefetch_l2_bytes(tx + f0, (size_t)(f1 - f0) * 8);
+    prefetch_l2_bytes(ty + f0, (size_t)(f1 - f0) * 8);
+    prefetch_l2_bytes(tz + f0, (size_t)(f1 - f0) * 8);
+    prefetch_l2_bytes(eoff + f0, (size_t)(f1 - f0) * 4);
+  }
   cp_wait<0>();
   __syncthreads();
   double* out = vb + (size_t)t * kBrickCells;
@@ -219,13 +243,20 @@ __global__ void __launch_bounds__(kLapThreads) k_laplace(const TileHdr* __restri
                                                          double* __restrict__ y, double diag,
                                                          double ih2,
                                                          const double* __restrict__ scale, int lds,
-                                                         const int* __restrict__ skip) {
+                                                         const int* __restrict__ skip, int pfd) {
   if (skip && *skip) return;
   __shared__ double E[1000];
   const int t = blockIdx.x, tid = threadIdx.x;
   const TileHdr* T = tiles + t;
   const int a0 = T->a0, a1 = T->a1;
   if (a0 == a1) return;
+  if (tid == kLapThreads - 32 && t + pfd < (int)gridDim.x) {  // a later CTA's tile into L2
+    const TileHdr* F = tiles + t + pfd;
+    const int f0 = F->a0, f1 = F->a1;
+    prefetch_l2_bytes(acell + f0, (size_t)(f1 - f0) * 2);
+    prefetch_l2_bytes(u + f0, (size_t)(f1 - f0) * 8);
+    prefetch_l2_bytes(vb + (size_t)(t + pfd) * kBrickCells, kBrickCells * 8);
+  }
   constexpr int kOut = kBrickCells / kLapThreads;
   // output nodes: up to kOut per thread
   int ac[kOut];
@@ -292,6 +323,16 @@ int apply_device_split(const cpm_band* b, double c, const double* u, const doubl
                        const double* scale, int lds, cudaStream_t s, const int* skip) {
   const double ih2 = 1.0 / (b->h * b->h);
   const double diag = c + 6.0 * ih2;
+  // L2 prefetch distance in tiles (both kernels): one wave of resident extend CTAs,
+  // 8 per SM (measured: 0.5x and 2x are slower; CPM_EXT_PFD / CPM_LAP_PFD override)
+  static const int pfd = [] {
+    const char* v = getenv("CPM_EXT_PFD");
+    if (v) return atoi(v);
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return 8 * sms;
+  }();
   {
     const int descCap = 512;
     const size_t smem = (size_t)b->maxBox * 8 + (size_t)descCap * 8;
@@ -306,7 +347,7 @@ int apply_device_split(const cpm_band* b, double c, const double* u, const doubl
     }                                                                                        \
     k_extend_nt<Z><<<b->nT, kNtThreads, smem, s>>>(b->tiles, b->maxBox, descCap, b->runs, u, uh, \
                                                    b->srcSplit, b->tx, b->ty, b->tz, b->eoff,   \
-                                                   b->vb, skip);                                \
+                                                   b->vb, skip, pfd);                           \
   } while (0)
     if (b->zeroFill) CPM_EXTNT(true); else CPM_EXTNT(false);
 #undef CPM_EXTNT
@@ -315,7 +356,9 @@ int apply_device_split(const cpm_band* b, double c, const double* u, const doubl
   {
     ProfScope ps(K_LAPLACE, s);
     // 128 threads per tile: 16 resident tiles per SM keep enough loads in flight
-    k_laplace<128><<<b->nT, 128, 0, s>>>(b->tiles, u, b->acell, b->vb, y, diag, ih2, scale, lds, skip);
+    static const int pfd2 = getenv("CPM_LAP_PFD") ? atoi(getenv("CPM_LAP_PFD")) : pfd;
+    k_laplace<128><<<b->nT, 128, 0, s>>>(b->tiles, u, b->acell, b->vb, y, diag, ih2, scale, lds, skip,
+                                         pfd2);
     count_launch();
   }
   CPM_CUDA(cudaGetLastError());
