@@ -206,6 +206,8 @@ __global__ void __launch_bounds__(kNtThreads, 8)
     prefetch_l2_bytes(ty + f0, (size_t)(f1 - f0) * 8);
     prefetch_l2_bytes(tz + f0, (size_t)(f1 - f0) * 8);
     prefetch_l2_bytes(eoff + f0, (size_t)(f1 - f0) * 4);
+    // and the header that lane will read one wave later
+    if (t + 2 * pfd < (int)gridDim.x) prefetch_l2_bytes(tiles + t + 2 * pfd, sizeof(TileHdr));
   }
   cp_wait<0>();
   __syncthreads();
