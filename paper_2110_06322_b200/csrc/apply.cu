@@ -90,12 +90,13 @@ __device__ __forceinline__ uint32_t ld_hint(const uint32_t* p, uint64_t pol) {
                : "l"(p), "l"(pol));
   return v;
 }
-// L2 prefetch of [p, p + bytes), widened to 16-byte granules (the arrays are
-// allocated with padding, so the rounding stays inside them).
+// L2 prefetch of the 16-byte granules inside [p, p + bytes) (rounded inward at the
+// end, so it never reaches past the array; the start rounds down by < 16 bytes
+// into the same allocation).
 __device__ __forceinline__ void prefetch_l2_bytes(const void* p, size_t bytes) {
-  if (bytes == 0) return;
   const uintptr_t a0 = (uintptr_t)p & ~(uintptr_t)15;
-  const uintptr_t a1 = ((uintptr_t)p + bytes + 15) & ~(uintptr_t)15;
+  const uintptr_t a1 = ((uintptr_t)p + bytes) & ~(uintptr_t)15;
+  if (a1 <= a0) return;
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(a0), "r"((unsigned)(a1 - a0))
                : "memory");
 }

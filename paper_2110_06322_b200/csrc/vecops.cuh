@@ -260,12 +260,12 @@ static __global__ void __launch_bounds__(TB) k_proj(Seg S, int k, const double* 
 //                  V_{j+1} <- (z - mu u_j - sum_i e_i Q_i) / rho
 //   (b = coef[0..j), e = coef[ldc .. ldc + j), rho = coef[2 ldc], mu = coef[2 ldc + 1];
 //   segment s reads coef + s * cstride)
-// L2 prefetch of [p, p + n) doubles (bulk, 16-byte granules; the vectors are
-// allocated with a stride padded to 64 doubles, so rounding stays inside them).
+// L2 prefetch of the 16-byte granules inside [p, p + n) doubles (bulk; rounded
+// inward at the end, the start rounds down by < 16 bytes into the same vector).
 __device__ __forceinline__ void prefetch_l2(const double* p, int64_t n) {
-  if (n <= 0) return;
   const uintptr_t a0 = (uintptr_t)p & ~(uintptr_t)15;
-  const uintptr_t a1 = ((uintptr_t)(p + n) + 15) & ~(uintptr_t)15;
+  const uintptr_t a1 = (uintptr_t)(p + n) & ~(uintptr_t)15;
+  if (n <= 0 || a1 <= a0) return;
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(a0), "r"((unsigned)(a1 - a0))
                : "memory");
 }
