@@ -249,16 +249,18 @@ __global__ void __launch_bounds__(kLapThreads) k_laplace(const TileHdr* __restri
                                                          const int* __restrict__ skip, int pfd) {
   if (skip && *skip) return;
   __shared__ double E[1000];
-  const int t = blockIdx.x, tid = threadIdx.x;
+  // tiles in reverse order: the extend's last tiles (their E u, u) are the ones
+  // still in L2 when this kernel starts
+  const int t = (int)gridDim.x - 1 - (int)blockIdx.x, tid = threadIdx.x;
   const TileHdr* T = tiles + t;
   const int a0 = T->a0, a1 = T->a1;
   if (a0 == a1) return;
-  if (tid == kLapThreads - 32 && t + pfd < (int)gridDim.x) {  // a later CTA's tile into L2
-    const TileHdr* F = tiles + t + pfd;
+  if (tid == kLapThreads - 32 && t - pfd >= 0) {  // a later CTA's tile into L2
+    const TileHdr* F = tiles + t - pfd;
     const int f0 = F->a0, f1 = F->a1;
     prefetch_l2_bytes(acell + f0, (size_t)(f1 - f0) * 2);
     prefetch_l2_bytes(u + f0, (size_t)(f1 - f0) * 8);
-    prefetch_l2_bytes(vb + (size_t)(t + pfd) * kBrickCells, kBrickCells * 8);
+    prefetch_l2_bytes(vb + (size_t)(t - pfd) * kBrickCells, kBrickCells * 8);
   }
   constexpr int kOut = kBrickCells / kLapThreads;
   // output nodes: up to kOut per thread
