@@ -147,7 +147,23 @@ int launch_dcgs_update(const vec::Seg& S, int k, double* V, int64_t ldv, const d
                        const double* coef, int ldc, int64_t cstride, cudaStream_t st,
                        const int* skip) {
   const int grid = S.nseg * S.gps;
-  if (k <= 64) {
+  static const bool reg = [] {
+    const char* v = getenv("CPM_UPD_REG");
+    return !v || *v != '0';
+  }();
+  if (reg && k - 1 <= 8) {
+    vec::k_dcgs_update_reg<256, 8><<<grid, 256, 0, st>>>(S, k, V, ldv, z, coef, ldc, cstride, skip);
+  } else if (reg && k - 1 <= 16) {
+    vec::k_dcgs_update_reg<256, 16><<<grid, 256, 0, st>>>(S, k, V, ldv, z, coef, ldc, cstride, skip);
+  } else if (reg && k - 1 <= 24) {
+    vec::k_dcgs_update_reg<256, 24><<<grid, 256, 0, st>>>(S, k, V, ldv, z, coef, ldc, cstride, skip);
+  } else if (reg && k - 1 <= 32) {
+    vec::k_dcgs_update_reg<256, 32><<<grid, 256, 0, st>>>(S, k, V, ldv, z, coef, ldc, cstride, skip);
+  } else if (reg && k - 1 <= 40) {
+    vec::k_dcgs_update_reg<256, 40><<<grid, 256, 0, st>>>(S, k, V, ldv, z, coef, ldc, cstride, skip);
+  } else if (reg && k - 1 <= 52) {
+    vec::k_dcgs_update_reg<256, 52><<<grid, 256, 0, st>>>(S, k, V, ldv, z, coef, ldc, cstride, skip);
+  } else if (k <= 64) {
     const size_t sm = ((size_t)k * (256 + 4) + 2 * (size_t)k) * sizeof(double);
     static bool attr = false;
     if (!attr) {

@@ -429,6 +429,60 @@ static __global__ void __launch_bounds__(TB) k_dcgs_update(Seg S, int k, double*
   }
 }
 
+// The same update with the basis elements loaded straight into registers (a
+// thread only ever uses its own element of each column): k - 1 <= KMAX, no
+// shared-memory staging; identical arithmetic order.
+template <int TB, int KMAX>
+static __global__ void __launch_bounds__(TB, 2) k_dcgs_update_reg(Seg S, int k, double* V, int64_t ldv,
+                                                                  const double* __restrict__ z,
+                                                                  const double* __restrict__ coef0,
+                                                                  int ldc, int64_t cstride,
+                                                                  const int* __restrict__ skip) {
+  if (skip && *skip) return;
+  __shared__ double cb[KMAX], ce[KMAX];
+  const int s = blockIdx.x / S.gps, lb = blockIdx.x % S.gps;
+  const int64_t o0 = S.off[s], n = S.off[s + 1] - o0;
+  const double* coef = coef0 + (size_t)s * cstride;  // this segment's coefficients
+  const int tid = threadIdx.x;
+  const int j = k - 1;
+  for (int i = tid; i < j; i += TB) {
+    cb[i] = coef[i];
+    ce[i] = coef[ldc + i];
+  }
+  const double rinv = 1.0 / coef[2 * ldc], mu = coef[2 * ldc + 1];
+  __syncthreads();
+  for (int64_t t0 = (int64_t)lb * TB; t0 < n; t0 += (int64_t)S.gps * TB) {
+    const int64_t e = t0 + tid;
+    if (e >= n) continue;
+    const double* p = V + o0 + e;
+    double q[KMAX];
+#pragma unroll
+    for (int i = 0; i < KMAX; ++i)
+      if (i < j) q[i] = __ldcg(p + (size_t)i * ldv);
+    const double uv = __ldcg(p + (size_t)j * ldv);
+    const double zv = __ldcg(z + o0 + e);
+    double sb0 = 0.0, sb1 = 0.0, se0 = 0.0, se1 = 0.0;
+#pragma unroll
+    for (int i = 0; i + 1 < KMAX; i += 2) {
+      if (i + 1 < j) {
+        sb0 += cb[i] * q[i];
+        sb1 += cb[i + 1] * q[i + 1];
+        se0 += ce[i] * q[i];
+        se1 += ce[i + 1] * q[i + 1];
+      } else if (i < j) {  // odd j: the last column
+        sb0 += cb[i] * q[i];
+        se0 += ce[i] * q[i];
+      }
+    }
+    if ((KMAX & 1) && KMAX - 1 < j) {  // unreachable for the even KMAX used
+      sb0 += cb[KMAX - 1] * q[KMAX - 1];
+      se0 += ce[KMAX - 1] * q[KMAX - 1];
+    }
+    V[(size_t)j * ldv + o0 + e] = (uv - (sb0 + sb1)) * rinv;
+    V[(size_t)(j + 1) * ldv + o0 + e] = (zv - mu * uv - (se0 + se1)) * rinv;
+  }
+}
+
 template <int TB>
 inline size_t proj_smem(int k) {
   return ((size_t)k * (TB + 4) + TB + (size_t)k + TB / 32) * sizeof(double);
