@@ -9,7 +9,9 @@ unit sphere, h = 1/200 (~4.1M band nodes), fp64:
 launching stream, max over ranks); `solve` reports the GMRES solve time.  The
 band is built once, outside the timed region (its build time is reported).
 Outside the timed steps, rank 0 also reports `config4_rd` (config-4 IMEX steps)
-and `config2_solve` (one config-2 RAS-FGMRES solve, ~40 s; --c2-kinner 0 skips it).
+and `config2_solve` (one config-2 RAS-FGMRES solve, ~40 s; --c2-kinner 0 skips it);
+with --c2-dist under torchrun (N | 8) every rank joins a partitioned config-2
+solve (`config2_solve_distributed`, max-over-ranks time).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
 
@@ -343,6 +345,38 @@ def run_mine(args):
         except Exception as e:  # report, never fail the main metric
             c2 = {"error": str(e)[:200]}
 
+    # N > 1: the same config-2 solve partitioned over the ranks (Morton slabs, NCCL
+    # halo exchange + allreduce, distributed RAS with n_sub = 8 a multiple of N)
+    c2d = None
+    if ws > 1 and args.c2_dist and args.c2_kinner > 0 and 8 % ws == 0:
+        try:
+            from paper_2110_06322_b200.distributed import DistributedCPM
+
+            cb = cpm.cpm_build_band("torus", 1.0 / 400, R=1.0, r=0.4)
+            cf = torch.empty(cb.n, dtype=torch.float64, device=dev)
+            cpm.cpm_eval_torus_rhs(cb, seeded_inputs.smooth_modulation_coeffs(1), cf)
+            D = DistributedCPM(cb)
+            dras = D.setup_ras(8, 4, args.c2_kinner, 1.0)
+            fo = cf[D.lo:D.hi].contiguous()
+            uo = torch.zeros_like(fo)
+            torch.distributed.barrier()
+            torch.cuda.synchronize()
+            ea = torch.cuda.Event(enable_timing=True)
+            eb = torch.cuda.Event(enable_timing=True)
+            ea.record(stream)
+            dst = D.solve(1.0, fo, uo, rtol=1e-10, restart=50, ras=dras)
+            eb.record(stream)
+            torch.cuda.synchronize()
+            tt = torch.tensor([ea.elapsed_time(eb) / 1e3], dtype=torch.float64, device=dev)
+            torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+            c2d = {"workload": "BASELINE configs[2] partitioned over the ranks (Morton slabs, NCCL), "
+                               f"RAS-FGMRES(50), 8 subdomains, overlap 4h, {args.c2_kinner} inner steps",
+                   "ranks": ws, "solve_s_max_over_ranks": float(tt.item()), "iterations": dst.iterations,
+                   "converged": bool(dst.converged), "resid_true_rel": dst.resid_true / dst.bnorm}
+            del dras, D, cb, cf, fo, uo
+        except Exception as e:  # report, never fail the main metric
+            c2d = {"error": str(e)[:200]}
+
     # e2e: same metric through the C ABI with HOST buffers (pinned), copies inside the timed region
     y_host = torch.empty(nA, dtype=torch.float64).pin_memory()
     u_np, y_np = u_host.numpy(), y_host.numpy()
@@ -425,6 +459,7 @@ def run_mine(args):
                     "d2h_bytes_per_step": 8 * nA * CFG["applies"]},
             "config4_rd": rd,
             "config2_solve": c2,
+            "config2_solve_distributed": c2d,
             "gpu_launches": launches,
             "clocks": clk,
         }
@@ -446,6 +481,9 @@ def main():
     ap.add_argument("--rd-steps", type=int, default=20, help="config-4 IMEX steps timed (0: skip)")
     ap.add_argument("--c2-kinner", type=int, default=16,
                     help="inner GMRES steps of the config-2 RAS solve (0: skip that solve)")
+    ap.add_argument("--c2-dist", action="store_true",
+                    help="under torchrun with N > 1 (N | 8): also time the config-2 solve "
+                         "partitioned over the ranks (NCCL); opt-in, untested on this pool")
     args = ap.parse_args()
     if args.warmup < 3:
         print("warning: --warmup < 3 violates the timing rules; using 3", file=sys.stderr)
