@@ -102,41 +102,6 @@ const bool g_force_cgs2 = [] {
 }();
 }  // namespace
 
-template <class Epi>
-static int launch_dcgs_dots_epi(const vec::Seg& S, int k, const double* V, int64_t ldv, const double* z,
-                                double* partial, int pld, double* out, int ldo, unsigned* counters,
-                                cudaStream_t st, const int* skip, Epi epi) {
-  const int grid = S.nseg * S.gps;
-  // ring depth: up to 4 stages within ~110 KB (2 blocks per SM)
-  auto depth = [](size_t stage) { return (int)std::max<size_t>(1, std::min<size_t>(4, (110 * 1024) / stage)); };
-  if (k <= 64) {
-    const size_t stage = (size_t)(k + 1) * (256 + 2 * vec::dots_threads_per_col(256, k)) * sizeof(double);
-    const int ns = depth(stage);
-    static bool attr = false;
-    if (!attr) {
-      CPM_CUDA(cudaFuncSetAttribute(vec::k_dcgs_dots<256, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    200 * 1024));
-      attr = true;
-    }
-    vec::k_dcgs_dots<256, Epi><<<grid, 256, ns * stage, st>>>(S, k, V, ldv, z, partial, pld, out, ldo,
-                                                              counters, skip, ns, epi);
-  } else {
-    const size_t stage = (size_t)(k + 1) * (128 + 2 * vec::dots_threads_per_col(128, k)) * sizeof(double);
-    const int ns = depth(stage);
-    static bool attr = false;
-    if (!attr) {
-      CPM_CUDA(cudaFuncSetAttribute(vec::k_dcgs_dots<128, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    200 * 1024));
-      attr = true;
-    }
-    vec::k_dcgs_dots<128, Epi><<<grid, 128, ns * stage, st>>>(S, k, V, ldv, z, partial, pld, out, ldo,
-                                                              counters, skip, ns, epi);
-  }
-  count_launch();
-  CPM_CUDA(cudaGetLastError());
-  return CPM_OK;
-}
-
 int launch_dcgs_dots(const vec::Seg& S, int k, const double* V, int64_t ldv, const double* z,
                      double* partial, int pld, double* out, int ldo, unsigned* counters,
                      cudaStream_t st, const int* skip) {

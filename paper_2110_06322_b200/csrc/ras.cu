@@ -259,20 +259,20 @@ __global__ void k_inner_init(InnerState* st, int S, int k) {
   q.kk = beta > 0.0 ? k : 0;
 }
 
-// Delayed-CGS2 step j of every segment's inner GMRES (one block per segment), the
-// arithmetic of krylov.cu k_dcgs_step without a convergence test: finalise column
-// j-1 ([cpend + b; rho], Givens), then the coefficients of the update pass.
-constexpr int kInnerStepThreads = 64;
-__global__ void __launch_bounds__(kInnerStepThreads) k_inner_dcgs_step(InnerState* st, int j) {
-  InnerState& q = st[blockIdx.x];
+// Delayed-CGS2 step j of one segment's inner GMRES, the arithmetic of krylov.cu
+// dcgs_step_body without a convergence test: finalise column j-1 ([cpend + b;
+// rho], Givens), then the coefficients of the update pass.  Run by the block (nt = blockDim.x <= 256 threads) of the segmented reduction
+// pass that completes segment s (InnerStepEpi): the inner solves are rank-local,
+// so no reduction sits between the pass and the step.
+__device__ void inner_step_body(InnerState& q, int j) {
   constexpr int ld = kMaxInner + 1, ldc = kMaxInner + 2;
-  const int k = j + 1, tid = threadIdx.x;
+  const int k = j + 1, tid = threadIdx.x, nt = blockDim.x;
   const double* b = q.red;
   const double* d = q.red + k;
-  __shared__ double sbb[kInnerStepThreads / 32], sbd[kInnerStepThreads / 32];
+  __shared__ double sbb[8], sbd[8];
   __shared__ int sstop;
   double pbb = 0.0, pbd = 0.0;
-  for (int i = tid; i < j; i += kInnerStepThreads) {
+  for (int i = tid; i < j; i += nt) {
     pbb += b[i] * b[i];
     pbd += b[i] * d[i];
   }
@@ -284,7 +284,7 @@ __global__ void __launch_bounds__(kInnerStepThreads) k_inner_dcgs_step(InnerStat
   }
   __syncthreads();
   double bb = 0.0, bd = 0.0;
-  for (int w = 0; w < kInnerStepThreads / 32; ++w) {
+  for (int w = 0; w < nt / 32; ++w) {
     bb += sbb[w];
     bd += sbd[w];
   }
@@ -293,7 +293,7 @@ __global__ void __launch_bounds__(kInnerStepThreads) k_inner_dcgs_step(InnerStat
   const bool brk = !(rho2 > 1e-28 * alpha);
   const double rho = brk ? 1.0 : sqrt(rho2);  // broken: the segment stops at kk = j
   if (j >= 1)
-    for (int i = tid; i < j; i += kInnerStepThreads) q.Hr[(size_t)(j - 1) * ld + i] = q.cpend[i] + b[i];
+    for (int i = tid; i < j; i += nt) q.Hr[(size_t)(j - 1) * ld + i] = q.cpend[i] + b[i];
   __syncthreads();
   if (tid == 0) {
     sstop = 0;
@@ -331,7 +331,7 @@ __global__ void __launch_bounds__(kInnerStepThreads) k_inner_dcgs_step(InnerStat
   double* cb = q.coef;
   double* ce = q.coef + ldc;
   if (sstop) {  // harmless coefficients for the (unused) rest of this segment
-    for (int i = tid; i < j; i += kInnerStepThreads) cb[i] = ce[i] = 0.0;
+    for (int i = tid; i < j; i += nt) cb[i] = ce[i] = 0.0;
     if (tid == 0) {
       q.coef[2 * ldc] = 1.0;
       q.coef[2 * ldc + 1] = 0.0;
@@ -339,13 +339,13 @@ __global__ void __launch_bounds__(kInnerStepThreads) k_inner_dcgs_step(InnerStat
     return;
   }
   const double mu = (gamma - bd) / rho2;
-  for (int l = tid; l <= j; l += kInnerStepThreads) {
+  for (int l = tid; l <= j; l += nt) {
     double gl = 0.0;  // (Hr b)_l
     for (int i = (l > 0 ? l - 1 : 0); i < j; ++i) gl += q.Hr[(size_t)i * ld + l] * b[i];
     const double ql = l < j ? d[l] : rho * mu;
     q.cpend[l] = (ql - gl) / rho;
   }
-  for (int i = tid; i < j; i += kInnerStepThreads) {
+  for (int i = tid; i < j; i += nt) {
     cb[i] = b[i];
     ce[i] = d[i] - mu * b[i];
   }
@@ -354,6 +354,11 @@ __global__ void __launch_bounds__(kInnerStepThreads) k_inner_dcgs_step(InnerStat
     q.coef[2 * ldc + 1] = mu;
   }
 }
+struct InnerStepEpi {
+  InnerState* st;
+  int j;
+  __device__ void operator()(int s) const { inner_step_body(st[s], j); }
+};
 
 __global__ void k_inner_lsq(InnerState* st) {
   InnerState& q = st[blockIdx.x];
@@ -725,15 +730,11 @@ int ras_apply_device(const cpm_ras* ras, const double* r, double* z, cudaStream_
   // update pass; step k only finalises the last Hessenberg column
   for (int j = 0; j <= k; ++j) {
     if (j < k) CPM_TRY(apply_device(&R->mb, ras->c, R->V + (size_t)j * R->ldv, R->W, nullptr, 0, s));
-    {
+    {  // the block that completes segment s's reduction runs its step (epilogue)
       ProfScope ps(K_MDOT, s);
-      CPM_TRY(launch_dcgs_dots(Sg, j + 1, R->V, R->ldv, R->W, R->partial, 2 * (kMaxInner + 2) + 8,
-                               base + o_red, lds, R->counters + S, s));
-    }
-    {
-      ProfScope ps(K_OTHER, s);
-      k_inner_dcgs_step<<<S, kInnerStepThreads, 0, s>>>(st, j);
-      count_launch();
+      CPM_TRY(launch_dcgs_dots_epi(Sg, j + 1, R->V, R->ldv, R->W, R->partial, 2 * (kMaxInner + 2) + 8,
+                                   base + o_red, lds, R->counters + S, s, nullptr,
+                                   InnerStepEpi{st, j}));
     }
     if (j < k) {
       ProfScope ps(K_CGS_UPDATE, s);
