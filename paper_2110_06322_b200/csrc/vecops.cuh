@@ -54,6 +54,31 @@ __device__ __forceinline__ double partial_sum(const double* partial, size_t base
   return warp_sum((a0 + a1) + (a2 + a3));
 }
 
+// partial_sum of two columns i, i2 at once (loads of both in flight); per column
+// the same order as partial_sum.
+__device__ __forceinline__ void partial_sum2(const double* partial, size_t base, int pld, int gps,
+                                             int i, int i2, int lane, double& r, double& r2) {
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0, c0 = 0.0, c1 = 0.0, c2 = 0.0, c3 = 0.0;
+  int b = lane;
+  for (; b + 96 < gps; b += 128) {
+    const double* p = partial + (base + b) * pld;
+    a0 += __ldcg(p + i);
+    c0 += __ldcg(p + i2);
+    a1 += __ldcg(p + 32 * (size_t)pld + i);
+    c1 += __ldcg(p + 32 * (size_t)pld + i2);
+    a2 += __ldcg(p + 64 * (size_t)pld + i);
+    c2 += __ldcg(p + 64 * (size_t)pld + i2);
+    a3 += __ldcg(p + 96 * (size_t)pld + i);
+    c3 += __ldcg(p + 96 * (size_t)pld + i2);
+  }
+  for (; b < gps; b += 32) {
+    a0 += __ldcg(partial + (base + b) * pld + i);
+    c0 += __ldcg(partial + (base + b) * pld + i2);
+  }
+  r = warp_sum((a0 + a1) + (a2 + a3));
+  r2 = warp_sum((c0 + c1) + (c2 + c3));
+}
+
 // Reduce acc[0..k) over the block into partial[blockIdx.x * pld + i]; then the
 // last block of the segment writes out[s*ldo + i] = scale_i * sum_b partial.
 template <int KMAX>
@@ -370,9 +395,20 @@ static __global__ void __launch_bounds__(TB) k_dcgs_dots(Seg S, int k, const dou
   __syncthreads();
   if (!last) return;
   __threadfence();
-  for (int i = warp; i < 2 * k; i += TB / 32) {
-    const double a = partial_sum(partial, (size_t)s * S.gps, pld, S.gps, i, lane);
-    if (lane == 0) out[(size_t)s * ldo + i] = a;
+  constexpr int NW = TB / 32;
+  for (int i = warp; i < 2 * k; i += 2 * NW) {  // two columns per warp at a time
+    const int i2 = i + NW;
+    if (i2 < 2 * k) {
+      double a, a2;
+      partial_sum2(partial, (size_t)s * S.gps, pld, S.gps, i, i2, lane, a, a2);
+      if (lane == 0) {
+        out[(size_t)s * ldo + i] = a;
+        out[(size_t)s * ldo + i2] = a2;
+      }
+    } else {
+      const double a = partial_sum(partial, (size_t)s * S.gps, pld, S.gps, i, lane);
+      if (lane == 0) out[(size_t)s * ldo + i] = a;
+    }
   }
   if (tid == 0) counters[s] = 0u;
   __syncthreads();  // out[] written by this block is visible to all its threads
