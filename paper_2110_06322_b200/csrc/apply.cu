@@ -148,6 +148,7 @@ __global__ void __launch_bounds__(kNtThreads, 8)
                 const double* __restrict__ ty, const double* __restrict__ tz,
                 const uint32_t* __restrict__ eoff, double* __restrict__ vb,
                 const int* __restrict__ skip, int pfd) {
+  pdl_wait();
   if (skip && *skip) return;
   extern __shared__ double smn[];
   double* box = smn;
@@ -247,6 +248,7 @@ __global__ void __launch_bounds__(kLapThreads) k_laplace(const TileHdr* __restri
                                                          double ih2,
                                                          const double* __restrict__ scale, int lds,
                                                          const int* __restrict__ skip, int pfd) {
+  pdl_wait();
   if (skip && *skip) return;
   __shared__ double E[1000];
   // tiles in reverse order: the extend's last tiles (their E u, u) are the ones
@@ -350,9 +352,10 @@ int apply_device_split(const cpm_band* b, double c, const double* u, const doubl
                                     227 * 1024));                                            \
       attr = true;                                                                           \
     }                                                                                        \
-    k_extend_nt<Z><<<b->nT, kNtThreads, smem, s>>>(b->tiles, b->maxBox, descCap, b->runs, u, uh, \
-                                                   b->srcSplit, b->tx, b->ty, b->tz, b->eoff,   \
-                                                   b->vb, skip, pfd);                           \
+    CPM_CUDA(launch_pdl(k_extend_nt<Z>, dim3((unsigned)b->nT), dim3(kNtThreads), smem, s,       \
+                        b->tiles, (int)b->maxBox, descCap, (const uint64_t*)b->runs, u, uh,     \
+                        (uint32_t)b->srcSplit, (const double*)b->tx, (const double*)b->ty,      \
+                        (const double*)b->tz, (const uint32_t*)b->eoff, b->vb, skip, pfd));     \
   } while (0)
     if (b->zeroFill) CPM_EXTNT(true); else CPM_EXTNT(false);
 #undef CPM_EXTNT
@@ -362,8 +365,9 @@ int apply_device_split(const cpm_band* b, double c, const double* u, const doubl
     ProfScope ps(K_LAPLACE, s);
     // 128 threads per tile: 16 resident tiles per SM keep enough loads in flight
     static const int pfd2 = getenv("CPM_LAP_PFD") ? atoi(getenv("CPM_LAP_PFD")) : pfd;
-    k_laplace<128><<<b->nT, 128, 0, s>>>(b->tiles, u, b->acell, b->vb, y, diag, ih2, scale, lds, skip,
-                                         pfd2);
+    CPM_CUDA(launch_pdl(k_laplace<128>, dim3((unsigned)b->nT), dim3(128), 0, s, b->tiles, u,
+                        (const uint16_t*)b->acell, (const double*)b->vb, y, diag, ih2, scale, lds,
+                        skip, pfd2));
     count_launch();
   }
   CPM_CUDA(cudaGetLastError());

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -68,6 +69,14 @@ void drain_pending() {
 }  // namespace
 
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* v = getenv("CPM_PDL");
+    return !v || *v != '0';
+  }();
+  return on;
+}
 
 ProfScope::ProfScope(KernelId id_, cudaStream_t s_) : id(id_), s(s_) {
   if (!g_prof_on) return;

@@ -5,6 +5,7 @@
 #include <stdint.h>
 
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/cpm.h"
@@ -45,6 +46,29 @@ struct ProfScope {
   cudaEvent_t a = nullptr, b = nullptr;
 };
 void count_launch();
+
+// Programmatic dependent launch for the per-step kernels (extend, laplace, the
+// two Krylov passes): the next kernel's CTAs are launched while the previous
+// grid drains and wait in pdl_wait() (griddepcontrol.wait: the predecessor has
+// completed and its writes are visible) before touching any data.  Every kernel
+// launched with launch_pdl calls pdl_wait() first.  CPM_PDL=0 disables it.
+bool pdl_enabled();
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 // ------------------------------------------------------------------ band data
 // One tile = one occupied 8^3 brick.  64-bit aligned, 168 bytes.

@@ -117,17 +117,23 @@ int launch_dcgs_update(const vec::Seg& S, int k, double* V, int64_t ldv, const d
     return !v || *v != '0';
   }();
   if (reg && k - 1 <= 8) {
-    vec::k_dcgs_update_reg<256, 8><<<grid, 256, 0, st>>>(S, k, V, ldv, z, coef, ldc, cstride, skip);
+    CPM_CUDA(launch_pdl(vec::k_dcgs_update_reg<256, 8>, dim3(grid), dim3(256), 0, st, S, k, V, ldv, z, coef,
+                        ldc, cstride, skip));
   } else if (reg && k - 1 <= 16) {
-    vec::k_dcgs_update_reg<256, 16><<<grid, 256, 0, st>>>(S, k, V, ldv, z, coef, ldc, cstride, skip);
+    CPM_CUDA(launch_pdl(vec::k_dcgs_update_reg<256, 16>, dim3(grid), dim3(256), 0, st, S, k, V, ldv, z, coef,
+                        ldc, cstride, skip));
   } else if (reg && k - 1 <= 24) {
-    vec::k_dcgs_update_reg<256, 24><<<grid, 256, 0, st>>>(S, k, V, ldv, z, coef, ldc, cstride, skip);
+    CPM_CUDA(launch_pdl(vec::k_dcgs_update_reg<256, 24>, dim3(grid), dim3(256), 0, st, S, k, V, ldv, z, coef,
+                        ldc, cstride, skip));
   } else if (reg && k - 1 <= 32) {
-    vec::k_dcgs_update_reg<256, 32><<<grid, 256, 0, st>>>(S, k, V, ldv, z, coef, ldc, cstride, skip);
+    CPM_CUDA(launch_pdl(vec::k_dcgs_update_reg<256, 32>, dim3(grid), dim3(256), 0, st, S, k, V, ldv, z, coef,
+                        ldc, cstride, skip));
   } else if (reg && k - 1 <= 40) {
-    vec::k_dcgs_update_reg<256, 40><<<grid, 256, 0, st>>>(S, k, V, ldv, z, coef, ldc, cstride, skip);
+    CPM_CUDA(launch_pdl(vec::k_dcgs_update_reg<256, 40>, dim3(grid), dim3(256), 0, st, S, k, V, ldv, z, coef,
+                        ldc, cstride, skip));
   } else if (reg && k - 1 <= 52) {
-    vec::k_dcgs_update_reg<256, 52><<<grid, 256, 0, st>>>(S, k, V, ldv, z, coef, ldc, cstride, skip);
+    CPM_CUDA(launch_pdl(vec::k_dcgs_update_reg<256, 52>, dim3(grid), dim3(256), 0, st, S, k, V, ldv, z, coef,
+                        ldc, cstride, skip));
   } else if (k <= 64) {
     const size_t sm = ((size_t)k * (256 + 4) + 2 * (size_t)k) * sizeof(double);
     static bool attr = false;

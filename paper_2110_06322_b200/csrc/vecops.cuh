@@ -330,6 +330,7 @@ static __global__ void __launch_bounds__(TB) k_dcgs_dots(Seg S, int k, const dou
                                                          int ldo, unsigned* counters,
                                                          const int* __restrict__ skip, int ns,
                                                          Epi epi = Epi()) {
+  pdl_wait();
   if (skip && *skip) return;
   extern __shared__ double smp[];  // ns stages of k + 1 columns (Q_0 .. Q_{j-1}, u_j, z)
   __shared__ bool last;
@@ -420,6 +421,7 @@ static __global__ void __launch_bounds__(TB) k_dcgs_update(Seg S, int k, double*
                                                            const double* __restrict__ z,
                                                            const double* __restrict__ coef0, int ldc,
                                                            int64_t cstride, const int* __restrict__ skip) {
+  pdl_wait();
   if (skip && *skip) return;
   constexpr int SV = TB + 4;
   extern __shared__ double smp[];
@@ -474,6 +476,7 @@ static __global__ void __launch_bounds__(TB, 2) k_dcgs_update_reg(Seg S, int k, 
                                                                   const double* __restrict__ coef0,
                                                                   int ldc, int64_t cstride,
                                                                   const int* __restrict__ skip) {
+  pdl_wait();
   if (skip && *skip) return;
   __shared__ double cb[KMAX], ce[KMAX];
   const int s = blockIdx.x / S.gps, lb = blockIdx.x % S.gps;
@@ -687,8 +690,8 @@ inline int launch_dcgs_dots_epi(const vec::Seg& S, int k, const double* V, int64
                                     200 * 1024));
       attr = true;
     }
-    vec::k_dcgs_dots<256, Epi><<<grid, 256, ns * stage, st>>>(S, k, V, ldv, z, partial, pld, out, ldo,
-                                                              counters, skip, ns, epi);
+    CPM_CUDA(launch_pdl(vec::k_dcgs_dots<256, Epi>, dim3(grid), dim3(256), ns * stage, st, S, k, V, ldv,
+                        z, partial, pld, out, ldo, counters, skip, ns, epi));
   } else {
     const size_t stage = (size_t)(k + 1) * (128 + 2 * vec::dots_threads_per_col(128, k)) * sizeof(double);
     const int ns = depth(stage);
