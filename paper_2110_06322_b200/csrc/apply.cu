@@ -148,8 +148,8 @@ __global__ void __launch_bounds__(kNtThreads, 8)
                 const double* __restrict__ ty, const double* __restrict__ tz,
                 const uint32_t* __restrict__ eoff, double* __restrict__ vb,
                 const int* __restrict__ skip, int pfd) {
-  pdl_wait();
-  if (skip && *skip) return;
+  // The band metadata (header, node offsets, run descriptors) is constant: it is
+  // requested before pdl_wait(); u is read and vb written only after it.
   extern __shared__ double smn[];
   double* box = smn;
   uint64_t* desc = (uint64_t*)(box + boxCells);
@@ -179,13 +179,22 @@ __global__ void __launch_bounds__(kNtThreads, 8)
     for (int c = tid; c < nbox; c += kNtThreads) box[c] = 0.0;
   }
   const int g = tid >> 3, l = tid & 7;
-  for (int c0 = r0; c0 < r1; c0 += descCap) {
-    const int nr = min(descCap, r1 - c0);
-    __syncthreads();  // previous round's descriptors consumed (and ZERO clear done)
-    for (int r = tid; r < nr; r += kNtThreads) cp_async8_hint(desc + r, runs + c0 + r, pfirst);
-    cp_commit();
+  int nr = min(descCap, r1 - r0);
+  for (int r = tid; r < nr; r += kNtThreads) cp_async8_hint(desc + r, runs + r0 + r, pfirst);
+  cp_commit();
+  pdl_wait();  // the predecessor grid (producer of u, reader of vb) has completed
+  if (skip && *skip) {
     cp_wait<0>();
-    __syncthreads();
+    return;
+  }
+  for (int c0 = r0; c0 < r1; c0 += nr, nr = min(descCap, r1 - c0)) {
+    if (c0 > r0) {
+      __syncthreads();  // previous round's descriptors consumed
+      for (int r = tid; r < nr; r += kNtThreads) cp_async8_hint(desc + r, runs + c0 + r, pfirst);
+      cp_commit();
+    }
+    cp_wait<0>();
+    __syncthreads();  // descriptors landed (and the ZERO clear done)
     for (int r = g; r < nr; r += kNtThreads / 8) {
       const uint64_t d = desc[r];
       const uint32_t src = (uint32_t)d, dst = (uint32_t)(d >> 32) & 0xffffu,
@@ -248,8 +257,6 @@ __global__ void __launch_bounds__(kLapThreads) k_laplace(const TileHdr* __restri
                                                          double ih2,
                                                          const double* __restrict__ scale, int lds,
                                                          const int* __restrict__ skip, int pfd) {
-  pdl_wait();
-  if (skip && *skip) return;
   __shared__ double E[1000];
   // tiles in reverse order: the extend's last tiles (their E u, u) are the ones
   // still in L2 when this kernel starts
@@ -265,16 +272,21 @@ __global__ void __launch_bounds__(kLapThreads) k_laplace(const TileHdr* __restri
     prefetch_l2_bytes(vb + (size_t)(t - pfd) * kBrickCells, kBrickCells * 8);
   }
   constexpr int kOut = kBrickCells / kLapThreads;
-  // output nodes: up to kOut per thread
+  // output nodes: up to kOut per thread; their cells (band metadata) are read
+  // before pdl_wait(), u and E u after it
   int ac[kOut];
   double au[kOut];
 #pragma unroll
   for (int k = 0; k < kOut; ++k) {
     const int a = a0 + tid + k * kLapThreads;
-    if (a < a1) {
-      ac[k] = __ldg(acell + a);
-      au[k] = __ldg(u + a);
-    }
+    if (a < a1) ac[k] = __ldg(acell + a);
+  }
+  pdl_wait();  // the extend (E u) and the producer of u have completed
+  if (skip && *skip) return;
+#pragma unroll
+  for (int k = 0; k < kOut; ++k) {
+    const int a = a0 + tid + k * kLapThreads;
+    if (a < a1) au[k] = __ldg(u + a);
   }
   // own eval cells (the only cells the extend wrote)
   const double* vt = vb + (size_t)t * kBrickCells;
