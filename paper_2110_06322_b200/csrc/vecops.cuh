@@ -16,6 +16,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdlib>
+
 #include "internal.cuh"
 
 namespace cpm {
@@ -416,6 +418,137 @@ static __global__ void __launch_bounds__(TB) k_dcgs_dots(Seg S, int k, const dou
   epi(s);
 }
 
+// ---- bulk-copy (TMA engine) variant of the reduction pass, single segment:
+// one thread arms an mbarrier with the tile's byte count and issues one
+// cp.async.bulk per column (2 KB) instead of one 8-byte cp.async per element;
+// the others wait on the mbarrier.  Column i of a stage at i * (TB + 4); every
+// thread sums the same elements in the same order as k_dcgs_dots's original
+// layout (bit-identical results).
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned cnt) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(b)), "r"(cnt) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(b)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+template <class Epi = NoEpi>
+static __global__ void __launch_bounds__(256) k_dcgs_dots_bulk(Seg S, int k, const double* __restrict__ V,
+                                                               int64_t ldv, const double* __restrict__ z,
+                                                               double* partial, int pld, double* out,
+                                                               int ldo, unsigned* counters,
+                                                               const int* __restrict__ skip, int ns,
+                                                               Epi epi = Epi()) {
+  constexpr int TB = 256, SVB = TB + 4;
+  pdl_wait();
+  if (skip && *skip) return;
+  extern __shared__ __align__(16) double smp[];
+  __shared__ __align__(8) uint64_t full[4];
+  __shared__ bool last;
+  const int s = blockIdx.x / S.gps, lb = blockIdx.x % S.gps;
+  const int64_t o0 = S.off[s], n = S.off[s + 1] - o0;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int P = dots_threads_per_col(TB, k);
+  const int col = tid / P, sub = tid % P;
+  const size_t stage = (size_t)(k + 1) * SVB;
+  const int64_t stride = (int64_t)S.gps * TB;
+  if (tid == 0) {
+    for (int q = 0; q < ns; ++q) mbar_init(&full[q], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int64_t t0, int q) {  // thread 0
+    if (t0 >= n) return;
+    const int cnt = (int)min((int64_t)TB, n - t0);
+    const unsigned bytes = (unsigned)((cnt + 1) & ~1) * 8u;  // 16-byte granules (padded vectors)
+    double* dst = smp + (size_t)q * stage;
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    mbar_expect_tx(&full[q], bytes * (unsigned)(k + 1));
+    for (int i = 0; i < k; ++i) bulk_g2s(dst + (size_t)i * SVB, V + (size_t)i * ldv + o0 + t0, bytes, &full[q]);
+    bulk_g2s(dst + (size_t)k * SVB, z + o0 + t0, bytes, &full[q]);
+  };
+  const int64_t tfirst = (int64_t)lb * TB;
+  if (tid == 0)
+    for (int q = 0; q < ns - 1; ++q) issue(tfirst + q * stride, q);
+  double a1 = 0.0, a2 = 0.0;
+  unsigned ph = 0;
+  int it = 0;
+  for (int64_t t0 = tfirst; t0 < n; t0 += stride, ++it) {
+    const int q = it % ns;
+    if (tid == 0) issue(t0 + (int64_t)(ns - 1) * stride, (it + ns - 1) % ns);
+    {  // the tile after the ring window: into L2 while this one is reduced
+      const int64_t tp = t0 + (int64_t)ns * stride;
+      if (tid <= k && tp < n) prefetch_l2((tid < k ? V + (size_t)tid * ldv : z) + o0 + tp, min((int64_t)TB, n - tp));
+    }
+    mbar_wait(&full[q], (ph >> q) & 1u);
+    ph ^= 1u << q;
+    double* sv = smp + (size_t)q * stage;
+    if (t0 + TB > n) {  // the last tile: elements past n read as 0 (as the staged zeros of k_dcgs_dots)
+      if (t0 + tid >= n)
+        for (int i = 0; i <= k; ++i) sv[(size_t)i * SVB + tid] = 0.0;
+      __syncthreads();
+    }
+    if (col < k) {
+      const double* c = sv + (size_t)col * SVB;
+      const double* su = sv + (size_t)(k - 1) * SVB;  // the lagged vector is the last column
+      const double* sz = sv + (size_t)k * SVB;
+      for (int e = sub; e < TB; e += P) {
+        const double cv = c[e];
+        a1 += cv * su[e];
+        a2 += cv * sz[e];
+      }
+    }
+    __syncthreads();  // the stage is refilled by the next issue
+  }
+  for (int o = P >> 1; o > 0; o >>= 1) {
+    a1 += __shfl_xor_sync(0xffffffffu, a1, o);
+    a2 += __shfl_xor_sync(0xffffffffu, a2, o);
+  }
+  if (sub == 0 && col < k) {
+    partial[(size_t)blockIdx.x * pld + col] = a1;
+    partial[(size_t)blockIdx.x * pld + k + col] = a2;
+  }
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) last = (atomicAdd(counters + s, 1u) == (unsigned)S.gps - 1u);
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  constexpr int NW = TB / 32;
+  for (int i = warp; i < 2 * k; i += 2 * NW) {
+    const int i2 = i + NW;
+    if (i2 < 2 * k) {
+      double a, a2v;
+      partial_sum2(partial, (size_t)s * S.gps, pld, S.gps, i, i2, lane, a, a2v);
+      if (lane == 0) {
+        out[(size_t)s * ldo + i] = a;
+        out[(size_t)s * ldo + i2] = a2v;
+      }
+    } else {
+      const double a = partial_sum(partial, (size_t)s * S.gps, pld, S.gps, i, lane);
+      if (lane == 0) out[(size_t)s * ldo + i] = a;
+    }
+  }
+  if (tid == 0) counters[s] = 0u;
+  __syncthreads();
+  epi(s);
+}
+
 template <int TB>
 static __global__ void __launch_bounds__(TB) k_dcgs_update(Seg S, int k, double* V, int64_t ldv,
                                                            const double* __restrict__ z,
@@ -681,7 +814,22 @@ inline int launch_dcgs_dots_epi(const vec::Seg& S, int k, const double* V, int64
   const int grid = S.nseg * S.gps;
   // ring depth: up to 4 stages within ~110 KB (2 blocks per SM)
   auto depth = [](size_t stage) { return (int)std::max<size_t>(1, std::min<size_t>(4, (110 * 1024) / stage)); };
-  if (k <= 64) {
+  static const bool bulk = [] {  // CPM_DOTS_BULK=0: the per-element cp.async kernel (A/B)
+    const char* v = getenv("CPM_DOTS_BULK");
+    return !v || *v != '0';
+  }();
+  if (bulk && k <= 64 && S.nseg == 1) {  // single segment: o0 = 0, 16-byte aligned column tiles
+    const size_t stage = (size_t)(k + 1) * (256 + 4) * sizeof(double);
+    const int ns = depth(stage);
+    static bool attrb = false;
+    if (!attrb) {
+      CPM_CUDA(cudaFuncSetAttribute(vec::k_dcgs_dots_bulk<Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    200 * 1024));
+      attrb = true;
+    }
+    CPM_CUDA(launch_pdl(vec::k_dcgs_dots_bulk<Epi>, dim3(grid), dim3(256), ns * stage, st, S, k, V, ldv,
+                        z, partial, pld, out, ldo, counters, skip, ns, epi));
+  } else if (k <= 64) {
     const size_t stage = (size_t)(k + 1) * (256 + 2 * vec::dots_threads_per_col(256, k)) * sizeof(double);
     const int ns = depth(stage);
     static bool attr = false;
