@@ -418,7 +418,7 @@ static __global__ void __launch_bounds__(TB) k_dcgs_dots(Seg S, int k, const dou
   epi(s);
 }
 
-// ---- bulk-copy (TMA engine) variant of the reduction pass, single segment:
+// ---- bulk-copy (TMA engine) variant of the reduction pass:
 // one thread arms an mbarrier with the tile's byte count and issues one
 // cp.async.bulk per column (2 KB) instead of one 8-byte cp.async per element;
 // the others wait on the mbarrier.  Column i of a stage at i * (TB + 4); every
@@ -472,15 +472,19 @@ static __global__ void __launch_bounds__(256) k_dcgs_dots_bulk(Seg S, int k, con
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
+  // A segment starting at an odd element is copied from one element earlier
+  // (16-byte aligned source) and read at offset sh = 1 in the stage.
+  const int sh = (int)(o0 & 1);
   auto issue = [&](int64_t t0, int q) {  // thread 0
     if (t0 >= n) return;
-    const int cnt = (int)min((int64_t)TB, n - t0);
+    const int cnt = (int)min((int64_t)TB, n - t0) + sh;
     const unsigned bytes = (unsigned)((cnt + 1) & ~1) * 8u;  // 16-byte granules (padded vectors)
     double* dst = smp + (size_t)q * stage;
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
     mbar_expect_tx(&full[q], bytes * (unsigned)(k + 1));
-    for (int i = 0; i < k; ++i) bulk_g2s(dst + (size_t)i * SVB, V + (size_t)i * ldv + o0 + t0, bytes, &full[q]);
-    bulk_g2s(dst + (size_t)k * SVB, z + o0 + t0, bytes, &full[q]);
+    for (int i = 0; i < k; ++i)
+      bulk_g2s(dst + (size_t)i * SVB, V + (size_t)i * ldv + o0 - sh + t0, bytes, &full[q]);
+    bulk_g2s(dst + (size_t)k * SVB, z + o0 - sh + t0, bytes, &full[q]);
   };
   const int64_t tfirst = (int64_t)lb * TB;
   if (tid == 0)
@@ -497,7 +501,7 @@ static __global__ void __launch_bounds__(256) k_dcgs_dots_bulk(Seg S, int k, con
     }
     mbar_wait(&full[q], (ph >> q) & 1u);
     ph ^= 1u << q;
-    double* sv = smp + (size_t)q * stage;
+    double* sv = smp + (size_t)q * stage + sh;
     if (t0 + TB > n) {  // the last tile: elements past n read as 0 (as the staged zeros of k_dcgs_dots)
       if (t0 + tid >= n)
         for (int i = 0; i <= k; ++i) sv[(size_t)i * SVB + tid] = 0.0;
@@ -818,7 +822,7 @@ inline int launch_dcgs_dots_epi(const vec::Seg& S, int k, const double* V, int64
     const char* v = getenv("CPM_DOTS_BULK");
     return !v || *v != '0';
   }();
-  if (bulk && k <= 64 && S.nseg == 1) {  // single segment: o0 = 0, 16-byte aligned column tiles
+  if (bulk && k <= 64) {
     const size_t stage = (size_t)(k + 1) * (256 + 4) * sizeof(double);
     const int ns = depth(stage);
     static bool attrb = false;
