@@ -51,7 +51,9 @@ def _gpu_band(cpm, kind, h, **kw):
 CASES = [("sphere", 0.1, {}), ("sphere", 0.13, {}), ("torus", 0.05, {"R": 1.0, "r": 0.4}),
          ("sphere", 0.06, {"R": 0.7}),
          ("sphere", 0.19, {}),  # coarsest spacing with lambda + h < reach: sparse, ragged tiles
-         ("sphere", 0.1, {"L": 1.2})]  # band clipped by the box [-L, L]^3 (stencils still inside)
+         ("sphere", 0.1, {"L": 1.2}),  # band clipped by the box [-L, L]^3 (stencils still inside)
+         ("sphere", 0.09, {"R": 1.3}),  # radius and spacing off the lattice
+         ("torus", 0.045, {"R": 1.2, "r": 0.5})]
 
 
 def _oracle_surface(kind, kw):
