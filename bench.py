@@ -348,9 +348,12 @@ def run_mine(args):
     # N > 1: the same config-2 solve partitioned over the ranks (Morton slabs, NCCL
     # halo exchange + allreduce, distributed RAS with n_sub = 8 a multiple of N)
     c2d = None
-    if ws > 1 and args.c2_dist and args.c2_kinner > 0 and 8 % ws == 0:
+    if args.c2_dist and args.c2_kinner > 0 and 8 % ws == 0 and "RANK" in os.environ:
         try:
             from paper_2110_06322_b200.distributed import DistributedCPM
+
+            if not torch.distributed.is_initialized():  # torchrun with one rank
+                torch.distributed.init_process_group("nccl")
 
             cb = cpm.cpm_build_band("torus", 1.0 / 400, R=1.0, r=0.4)
             cf = torch.empty(cb.n, dtype=torch.float64, device=dev)
@@ -464,7 +467,7 @@ def run_mine(args):
             "clocks": clk,
         }
         print(json.dumps(line), flush=True)
-    if ws > 1:
+    if torch.distributed.is_available() and torch.distributed.is_initialized():
         torch.distributed.destroy_process_group()
     return 0
 
@@ -482,8 +485,8 @@ def main():
     ap.add_argument("--c2-kinner", type=int, default=16,
                     help="inner GMRES steps of the config-2 RAS solve (0: skip that solve)")
     ap.add_argument("--c2-dist", action="store_true",
-                    help="under torchrun with N > 1 (N | 8): also time the config-2 solve "
-                         "partitioned over the ranks (NCCL); opt-in, untested on this pool")
+                    help="under torchrun (N | 8): also time the config-2 solve partitioned over "
+                         "the ranks (NCCL); opt-in, run here with one rank only")
     args = ap.parse_args()
     if args.warmup < 3:
         print("warning: --warmup < 3 violates the timing rules; using 3", file=sys.stderr)
