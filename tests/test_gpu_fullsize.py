@@ -1,4 +1,4 @@
-"""Full-size BASELINE configs 2 and 3 on the GPU, checked against the oracle on
+"""Full-size BASELINE configs 2, 3 and 4 on the GPU, checked against the oracle on
 sampled outputs (the oracle's row formula works at any size) and by properties
 that hold at any size.
 
@@ -6,6 +6,8 @@ config 2: torus R=1 r=0.4, h=1/400 (20.9M active nodes), c=1, torus rhs (seed 1)
           RAS(8 Morton slabs, overlap 4)-FGMRES(50), rtol 1e-10.
 config 3: unit sphere h=1/800 (~66M active nodes), c=0.1, f = Y_10^5 + 1e-3 N(0,1)
           (seed 2): band, rhs and apply at full size; a bounded RAS-FGMRES run.
+config 4: Schnakenberg IMEX Euler on the config-2 torus: one step, both shifted
+          systems checked on sampled rows.
 """
 import numpy as np
 import pytest
@@ -109,3 +111,29 @@ def test_config3_full_size(cpm):
     u = torch.zeros_like(f)
     st = cpm.cpm_solve(band, c, f, u, rtol=1e-10, restart=50, maxit=50, ras=ras)
     assert st.iterations == 50 and st.resid_true < 0.5 * st.bnorm
+
+
+def test_config4_full_size(cpm):
+    """config 4 (Schnakenberg IMEX Euler, torus h = 1/400, 20.9M nodes): one GPU step,
+    then both shifted systems (c_i - Delta_S^h) w1 = c_i (w0 + dt R_w(u0, v0)) checked
+    on sampled rows with the oracle's reaction and row formula (reading R14)."""
+    from oracle.reaction import SchnakenbergParams, imex_rhs, initial_state
+
+    h = 1.0 / 400
+    surf = Torus(1.0, 0.4)
+    p = SchnakenbergParams()
+    band = cpm.cpm_build_band("torus", h, R=1.0, r=0.4)
+    assert band.n > 20_000_000
+    ga = cpm.cpm_band_active_coords(band).astype(np.int64)
+    u0, v0 = initial_state(None, p, seed=3, ijk=ga)
+    u = torch.from_numpy(u0).cuda()
+    v = torch.from_numpy(v0).cuda()
+    s1, s2 = cpm.cpm_rd_step(band, u, v)
+    torch.cuda.synchronize()
+    assert s1.converged and s2.converged
+    fu, fv = imex_rhs(u0, v0, p)
+    sel = np.random.default_rng(7).choice(band.n, 300, replace=False)
+    for w1, f, mu in ((u.cpu().numpy(), fu, p.mu1), (v.cpu().numpy(), fv, p.mu2)):
+        c = 1.0 / (p.dt * mu)
+        r = f[sel] - apply_rows(_B(surf, h), c, _lookup(ga, w1), ga[sel])
+        assert np.abs(r).max() <= 1e-8 * np.abs(f).max()
