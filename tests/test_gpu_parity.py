@@ -264,6 +264,24 @@ def test_solve_host_pointers_and_x0(cpm):
     assert st2.iterations <= 3
 
 
+def test_solve_degenerate_cases(cpm):
+    """f = 0: u = 0 without an Arnoldi step; maxit reached: not converged, no error,
+    the returned u still reduces the residual; restart = 1 (GMRES(1)) converges."""
+    gb = _gpu_band(cpm, "sphere", 0.1)
+    z = torch.zeros(gb.n, dtype=torch.float64, device="cuda")
+    u = torch.zeros_like(z)
+    st = cpm.cpm_solve(gb, 1.0, z, u, rtol=1e-10, restart=30)
+    assert st.converged and st.iterations == 0 and torch.count_nonzero(u).item() == 0
+    f = torch.empty_like(z)
+    cpm.cpm_eval_sph(gb, 3, 2, 13.0, f)
+    u.zero_()
+    st = cpm.cpm_solve(gb, 1.0, f, u, rtol=1e-10, restart=30, maxit=5)
+    assert not st.converged and st.iterations == 5 and st.resid_true < st.bnorm
+    u.zero_()
+    st = cpm.cpm_solve(gb, 10.0, f, u, rtol=1e-8, restart=1, maxit=20000)
+    assert st.converged and st.resid_true <= 2e-8 * st.bnorm
+
+
 # ------------------------------------------------------------------ full size (config 1)
 @pytest.fixture(scope="module")
 def big(cpm):
