@@ -576,7 +576,11 @@ static __global__ void __launch_bounds__(TB) k_dcgs_update(Seg S, int k, double*
   }
   const double rinv = 1.0 / coef[2 * ldc], mu = coef[2 * ldc + 1];
   __syncthreads();
-  for (int64_t t0 = (int64_t)lb * TB; t0 < n; t0 += (int64_t)S.gps * TB) {
+  // tiles from the block's last to its first: the reduction pass before this one
+  // ended on the high tiles, which are still in L2 (each element is independent)
+  const int64_t stride = (int64_t)S.gps * TB, tf = (int64_t)lb * TB;
+  const int64_t tl = tf < n ? tf + (n - 1 - tf) / stride * stride : tf - stride;
+  for (int64_t t0 = tl; t0 >= tf; t0 -= stride) {
     const int64_t e = t0 + tid;
     if (e >= n) continue;
     const double* p = V + o0 + e;
@@ -627,7 +631,11 @@ static __global__ void __launch_bounds__(TB, 2) k_dcgs_update_reg(Seg S, int k, 
   }
   const double rinv = 1.0 / coef[2 * ldc], mu = coef[2 * ldc + 1];
   __syncthreads();
-  for (int64_t t0 = (int64_t)lb * TB; t0 < n; t0 += (int64_t)S.gps * TB) {
+  // tiles from the block's last to its first: the reduction pass before this one
+  // ended on the high tiles, which are still in L2 (each element is independent)
+  const int64_t stride = (int64_t)S.gps * TB, tf = (int64_t)lb * TB;
+  const int64_t tl = tf < n ? tf + (n - 1 - tf) / stride * stride : tf - stride;
+  for (int64_t t0 = tl; t0 >= tf; t0 -= stride) {
     const int64_t e = t0 + tid;
     if (e >= n) continue;
     const double* p = V + o0 + e;
