@@ -340,6 +340,7 @@ int apply_device(const cpm_band* b, double c, const double* u, double* y, const 
 
 int apply_device_split(const cpm_band* b, double c, const double* u, const double* uh, double* y,
                        const double* scale, int lds, cudaStream_t s, const int* skip) {
+  if (b->nT == 0) return CPM_OK;  // no tiles (an empty sub-band): nothing to write
   const double ih2 = 1.0 / (b->h * b->h);
   const double diag = c + 6.0 * ih2;
   // L2 prefetch distance in tiles (both kernels): one wave of resident extend CTAs,
