@@ -134,7 +134,7 @@ int launch_dcgs_update(const vec::Seg& S, int k, double* V, int64_t ldv, const d
   } else if (reg && k - 1 <= 52) {
     CPM_CUDA(launch_pdl(vec::k_dcgs_update_reg<256, 52>, dim3(grid), dim3(256), 0, st, S, k, V, ldv, z, coef,
                         ldc, cstride, skip));
-  } else if (k <= 64) {
+  } else if (k <= 52) {  // CPM_UPD_REG=0 (A/B)
     const size_t sm = ((size_t)k * (256 + 4) + 2 * (size_t)k) * sizeof(double);
     static bool attr = false;
     if (!attr) {
@@ -143,7 +143,7 @@ int launch_dcgs_update(const vec::Seg& S, int k, double* V, int64_t ldv, const d
       attr = true;
     }
     vec::k_dcgs_update<256><<<grid, 256, sm, st>>>(S, k, V, ldv, z, coef, ldc, cstride, skip);
-  } else {
+  } else {  // 128-element tiles: two blocks per SM still fit (results do not depend on the tile)
     const size_t sm = ((size_t)k * (128 + 4) + 2 * (size_t)k) * sizeof(double);
     static bool attr = false;
     if (!attr) {

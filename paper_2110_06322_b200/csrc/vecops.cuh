@@ -830,7 +830,7 @@ inline int launch_dcgs_dots_epi(const vec::Seg& S, int k, const double* V, int64
     const char* v = getenv("CPM_DOTS_BULK");
     return !v || *v != '0';
   }();
-  if (bulk && k <= 64) {
+  if (bulk && k <= 52) {  // a stage of (k+1) 2 KB columns: two blocks per SM
     const size_t stage = (size_t)(k + 1) * (256 + 4) * sizeof(double);
     const int ns = depth(stage);
     static bool attrb = false;
@@ -841,7 +841,7 @@ inline int launch_dcgs_dots_epi(const vec::Seg& S, int k, const double* V, int64
     }
     CPM_CUDA(launch_pdl(vec::k_dcgs_dots_bulk<Epi>, dim3(grid), dim3(256), ns * stage, st, S, k, V, ldv,
                         z, partial, pld, out, ldo, counters, skip, ns, epi));
-  } else if (k <= 64) {
+  } else if (k <= 51) {  // CPM_DOTS_BULK=0 (A/B)
     const size_t stage = (size_t)(k + 1) * (256 + 2 * vec::dots_threads_per_col(256, k)) * sizeof(double);
     const int ns = depth(stage);
     static bool attr = false;

@@ -264,6 +264,25 @@ def test_solve_host_pointers_and_x0(cpm):
     assert st2.iterations <= 3
 
 
+def test_solve_parity_large_restart(cpm):
+    """GMRES(64): the Krylov passes for k > 52 columns (128-element tiles)."""
+    h, c = 0.1, 1.0
+    gb = _gpu_band(cpm, "sphere", h)
+    ob = OBand(Sphere(1.0), h)
+    ga = cpm.cpm_band_active_coords(gb).astype(np.int64)
+    perm = _perm_to_oracle(ga, ob)
+    f = torch.empty(gb.n, dtype=torch.float64, device="cuda")
+    cpm.cpm_eval_sph(gb, 3, 2, c + 12.0, f)
+    u = torch.zeros_like(f)
+    st = cpm.cpm_solve(gb, c, f, u, rtol=1e-10, restart=64)
+    A = shifted_operator(ob, c)
+    xo, so = ogmres(lambda v: A @ v, rhs_sph(ob, c, 3, 2), restart=64, rtol=1e-10)
+    assert st.converged and so.converged
+    assert abs(st.iterations - so.iterations) <= 1, (st.iterations, so.iterations)
+    err = np.abs(u.cpu().numpy() - xo[perm]).max() / np.abs(xo).max()
+    assert err <= SOLVE_TOL, err
+
+
 def test_solve_degenerate_cases(cpm):
     """f = 0: u = 0 without an Arnoldi step; maxit reached: not converged, no error,
     the returned u still reduces the residual; restart = 1 (GMRES(1)) converges."""
