@@ -134,6 +134,9 @@ int launch_dcgs_update(const vec::Seg& S, int k, double* V, int64_t ldv, const d
   } else if (reg && k - 1 <= 52) {
     CPM_CUDA(launch_pdl(vec::k_dcgs_update_reg<256, 52>, dim3(grid), dim3(256), 0, st, S, k, V, ldv, z, coef,
                         ldc, cstride, skip));
+  } else if (reg && k - 1 <= 64) {  // one block per SM, up to 64 loads in flight per thread
+    CPM_CUDA(launch_pdl(vec::k_dcgs_update_reg<256, 64, 1>, dim3(grid), dim3(256), 0, st, S, k, V, ldv, z,
+                        coef, ldc, cstride, skip));
   } else if (k <= 52) {  // CPM_UPD_REG=0 (A/B)
     const size_t sm = ((size_t)k * (256 + 4) + 2 * (size_t)k) * sizeof(double);
     static bool attr = false;

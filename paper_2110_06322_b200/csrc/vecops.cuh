@@ -611,8 +611,8 @@ static __global__ void __launch_bounds__(TB) k_dcgs_update(Seg S, int k, double*
 // The same update with the basis elements loaded straight into registers (a
 // thread only ever uses its own element of each column): k - 1 <= KMAX, no
 // shared-memory staging; identical arithmetic order.
-template <int TB, int KMAX>
-static __global__ void __launch_bounds__(TB, 2) k_dcgs_update_reg(Seg S, int k, double* V, int64_t ldv,
+template <int TB, int KMAX, int MINB = 2>
+static __global__ void __launch_bounds__(TB, MINB) k_dcgs_update_reg(Seg S, int k, double* V, int64_t ldv,
                                                                   const double* __restrict__ z,
                                                                   const double* __restrict__ coef0,
                                                                   int ldc, int64_t cstride,
