@@ -202,6 +202,27 @@ def test_semidiscrete_2d_golden_on_plane():
             assert abs(y_z) == 0.0                   # off-plane values are never read
 
 
+def test_offlattice_plane_golden_rows():
+    """Eq. 4 on a plane between lattice planes (z0 = h/2, h/4), where
+    u != E u so the stabilisation term -(6/h^2)(I - E) is exercised; values derived by
+    hand in tests/golden/offlattice_plane.txt.  Pins the sign and weight of that term
+    (the row formula apply_rows; test_apply_rows_equals_assembled_matrix ties the
+    assembled matrix to it)."""
+    rows = _golden("offlattice_plane.txt")
+    for h in (0.25, 0.1):
+        for t, si, sj, sk, pi, pj, pk, val in rows:
+            class _B:
+                pass
+
+            _B.h = h
+            _B.surface = Plane(t * h)
+            src = np.array([si, sj, sk], dtype=np.int64)
+            probe = np.array([[pi, pj, pk]], dtype=np.int64)
+            u_delta = lambda ijk: np.all(ijk == src[None, :], axis=1).astype(float)
+            y = apply_rows(_B, 0.0, u_delta, probe)[0]      # (c I - Delta_S^h) u, c = 0
+            assert abs(-y * h * h - val) <= 1e-12 * max(1.0, abs(val)), (t, si, sj, sk, pi, pj, pk)
+
+
 def test_constants_in_kernel():
     b = Band(Sphere(1.0), 0.1)
     L = laplace_beltrami_matrix(b)
@@ -316,6 +337,31 @@ def test_arnoldi_fixed_full_dimension_is_exact():
     assert np.allclose(A @ z, r, atol=1e-10)
 
 
+def test_arnoldi_fixed_minimises_residual_over_krylov_space():
+    """k < n GMRES steps (reading R6): z_k = argmin_{z in K_k(A, b)} ||b - A z||_2.
+    Checked against an independent least-squares fit on the explicit (column-normalised)
+    Krylov basis [b, Ab, ..., A^{k-1} b] (the defining property of GMRES, Saad §6.5.1);
+    a FOM (Galerkin) solve of the square Hessenberg system gives a larger residual."""
+    rng = np.random.default_rng(11)
+    n = 40
+    A = rng.normal(size=(n, n)) + 4 * np.eye(n)
+    b = rng.normal(size=n)
+    for k in (1, 2, 3, 5, 8):
+        z = arnoldi_fixed(lambda v: A @ v, b, k)
+        K = np.empty((n, k))
+        v = b.copy()
+        for q in range(k):
+            K[:, q] = v / np.linalg.norm(v)
+            v = A @ K[:, q]
+        coef, *_ = np.linalg.lstsq(A @ K, b, rcond=None)
+        r_min = np.linalg.norm(b - A @ (K @ coef))
+        r_z = np.linalg.norm(b - A @ z)
+        assert abs(r_z - r_min) <= 1e-10 * np.linalg.norm(b), k
+        # z lies in K_k(A, b)
+        c2, *_ = np.linalg.lstsq(K, z, rcond=None)
+        assert np.linalg.norm(K @ c2 - z) <= 1e-9 * np.linalg.norm(z)
+
+
 # ---------------------------------------------------------------- RAS (§2.2)
 def test_order_key_hand_values():
     k = band_order_key(np.array([[0, 0, 0], [1, 0, 0], [0, 1, 0], [0, 0, 1], [8, 0, 0], [-1, 0, 0]]))
@@ -338,6 +384,49 @@ def test_partition_and_overlap_invariants():
     o4 = grow_overlap(b, dis[3], 4)
     assert set(dis[3]).issubset(o2) and set(o2).issubset(o4)
     assert slab_bounds(10, 3) == [0, 3, 6, 10]
+
+
+def test_overlap_equals_graph_distance_ball():
+    """Reading R7 (-mesh_nover 4): S_j = the active nodes within
+    lattice 6-neighbour graph distance N_O of S~_j, checked with an independent
+    shortest-path computation (scipy.sparse.csgraph) on the active adjacency graph."""
+    import scipy.sparse as sps
+    from scipy.sparse.csgraph import shortest_path
+
+    b = Band(Sphere(1.0), 0.2)
+    key = {tuple(p): n for n, p in enumerate(b.active.tolist())}
+    ri, ci = [], []
+    for n, (i, j, k) in enumerate(b.active.tolist()):
+        for d in ((1, 0, 0), (-1, 0, 0), (0, 1, 0), (0, -1, 0), (0, 0, 1), (0, 0, -1)):
+            m = key.get((i + d[0], j + d[1], k + d[2]))
+            if m is not None:
+                ri.append(n)
+                ci.append(m)
+    G = sps.csr_matrix((np.ones(len(ri)), (ri, ci)), shape=(b.nA, b.nA))
+    dis = disjoint_subdomains(b, 4)
+    for s in (0, 2):
+        D = shortest_path(G, unweighted=True, indices=dis[s]).min(axis=0)
+        for layers in (0, 1, 2, 4):
+            want = np.nonzero(D <= layers)[0]
+            got = grow_overlap(b, dis[s], layers)
+            assert np.array_equal(np.sort(got), want), (s, layers)
+
+
+def test_ras_stationary_iteration_converges_to_solution():
+    """Eq. 5-6 with Dirichlet transmission and exact local solves,
+    iterated as a stationary method u^{n+1} = u^n + M (f - A u^n), converges to the
+    single-domain solution A^{-1} f (restricted prolongation u^{n+1} = sum_j u_j|_{S~_j});
+    an additive prolongation (sum over the overlapping S_j) over-corrects the overlap
+    and does not."""
+    b = Band(Sphere(1.0), 0.16)
+    A = shifted_operator(b, 1.0)
+    f = rhs_sph(b, 1.0, 3, 2)
+    x = spla.spsolve(A.tocsc(), f)
+    M = RAS(b, A, nsub=4, overlap=2, local="exact")
+    u = np.zeros(b.nA)
+    for _ in range(60):
+        u = u + M(f - A @ u)
+    assert np.abs(u - x).max() <= 1e-8 * np.abs(x).max()
 
 
 def test_ras_single_subdomain_exact_is_inverse():
