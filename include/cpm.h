@@ -22,6 +22,13 @@
  *    a result must reach the host (cpm_solve statistics, host outputs).
  *  - Handles (cpm_band, cpm_ras, cpm_comm) are owned by the caller and
  *    released with the matching *_free; they own all device memory they use.
+ *  - Concurrency: a band (and every cpm_ras / cpm_part built on it) owns ONE
+ *    set of scratch buffers (E u bricks, host staging, the GMRES workspace).
+ *    Calls on the same band must be issued one stream at a time from one
+ *    thread; concurrent calls on one band from different streams or threads
+ *    race.  Different bands are independent.
+ *  - The partitioned calls (cpm_part_*, cpm_part_ras_*) take DEVICE pointers
+ *    only; a host pointer returns CPM_ERR_ARG.
  *  - Only p = 3 (tricubic) interpolation and d = 3 are implemented.
  */
 #ifndef CPM_H_
@@ -136,8 +143,11 @@ int cpm_apply(const cpm_band* band, double c, const double* u, double* y, void* 
  * x0 = 0) and the solution on exit; convergence when the Givens residual
  * estimate <= rtol * ||f||_2; maxit bounds the total Arnoldi steps.
  * f, u: nA doubles (device or host).  stats may be NULL.  Synchronises `stream`.
- * Errors: CPM_ERR_ARG (restart < 1 or > 128, rtol <= 0), CPM_ERR_CUDA,
- * CPM_ERR_NOMEM. Not converging within maxit is NOT an error (stats.converged = 0). */
+ * Errors: CPM_ERR_ARG (restart < 1 or > 128, rtol <= 0, f not finite), CPM_ERR_CUDA,
+ * CPM_ERR_NOMEM. Not converging within maxit is NOT an error (stats.converged = 0).
+ * A restart cycle that completes no Arnoldi step (non-finite x0 or residual) or a
+ * non-finite residual estimate ends the solve with stats.breakdown = 1,
+ * stats.converged = 0 (never an endless restart loop). */
 int cpm_solve(const cpm_band* band, double c, const double* f, double* u, double rtol, int restart,
               int maxit, const cpm_ras* ras, cpm_solve_stats* stats, void* stream);
 

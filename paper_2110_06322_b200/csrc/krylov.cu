@@ -421,6 +421,7 @@ int gmres_device(const LinOp& A, const PrecOp* M, const double* b, double* x, in
   CPM_CUDA(cudaMemcpyAsync(&ws.hst->est, &st->beta2, sizeof(double), cudaMemcpyDeviceToHost, s));
   CPM_CUDA(cudaStreamSynchronize(s));
   const double bnorm = sqrt(ws.hst->est);
+  if (!std::isfinite(bnorm)) return fail(CPM_ERR_ARG, "cpm_solve: right-hand side is not finite");
   const double target = rtol * bnorm;
   CPM_CUDA(cudaMemcpyAsync(&st->target, &target, sizeof(double), cudaMemcpyHostToDevice, s));
   CPM_CUDA(cudaMemsetAsync(&st->its, 0, sizeof(int), s));
@@ -450,6 +451,7 @@ int gmres_device(const LinOp& A, const PrecOp* M, const double* b, double* x, in
     }
     if (its >= maxit) break;
     ++cycles;
+    const int its_cycle0 = its;
     if (!flex && !g_force_cgs2) {
       // delayed CGS2: V_0 = r / beta is the first lagged vector
       {
@@ -553,6 +555,12 @@ int gmres_device(const LinOp& A, const PrecOp* M, const double* b, double* x, in
       break;
     }
     if (its >= maxit) break;
+    // no Arnoldi step completed (a breakdown at j = 0: a non-finite x0 or residual)
+    // or a non-finite estimate: restarting cannot make progress, stop and report it
+    if (its == its_cycle0 || !std::isfinite(est)) {
+      breakdown = 1;
+      break;
+    }
   }
   double rtrue = 0.0;
   if (stats) {

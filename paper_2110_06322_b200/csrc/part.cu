@@ -488,12 +488,16 @@ int cpm_part_apply_local(const cpm_part* p, double c, const double* u_owned, con
                          double* y_owned, void* stream) {
   if (!p || !u_owned || !y_owned || (p->nHalo > 0 && !u_halo))
     return fail(CPM_ERR_ARG, "cpm_part_apply_local: null argument");
+  if (!is_device_ptr(u_owned) || !is_device_ptr(y_owned) || (p->nHalo > 0 && !is_device_ptr(u_halo)))
+    return fail(CPM_ERR_ARG, "cpm_part_apply_local: vectors must be device memory");
   return apply_device_split(&p->lb, c, u_owned, u_halo, y_owned, nullptr, 0, (cudaStream_t)stream);
 }
 
 int cpm_part_apply(const cpm_part* p, const cpm_comm* comm, double c, const double* u_owned,
                    double* y_owned, void* stream) {
   if (!p || !u_owned || !y_owned) return fail(CPM_ERR_ARG, "cpm_part_apply: null argument");
+  if (!is_device_ptr(u_owned) || !is_device_ptr(y_owned))
+    return fail(CPM_ERR_ARG, "cpm_part_apply: vectors must be device memory");
   cudaStream_t s = (cudaStream_t)stream;
   CPM_TRY(part_exchange(p, comm, u_owned, s));
   return apply_device_split(&p->lb, c, u_owned, p->hbuf, y_owned, nullptr, 0, s);
@@ -503,6 +507,8 @@ int cpm_part_solve(const cpm_part* p, const cpm_comm* comm, double c, const doub
                    double* u_owned, double rtol, int restart, int maxit, const cpm_ras* ras,
                    cpm_solve_stats* stats, void* stream) {
   if (!p || !f_owned || !u_owned) return fail(CPM_ERR_ARG, "cpm_part_solve: null argument");
+  if (!is_device_ptr(f_owned) || !is_device_ptr(u_owned))
+    return fail(CPM_ERR_ARG, "cpm_part_solve: vectors must be device memory");
   if (p->nranks > 1 && !comm) return fail(CPM_ERR_ARG, "cpm_part_solve: needs a communicator");
   PrecOp M;
   if (ras) {

@@ -844,12 +844,16 @@ int cpm_part_ras_apply_local(const cpm_ras* ras, const double* r_owned, const do
   if (!ras || !r_owned || !z_owned) return fail(CPM_ERR_ARG, "cpm_part_ras_apply_local: null argument");
   const RasImpl* R = (const RasImpl*)ras->impl;
   if (R->nHalo > 0 && !r_halo) return fail(CPM_ERR_ARG, "cpm_part_ras_apply_local: null halo");
+  if (!is_device_ptr(r_owned) || !is_device_ptr(z_owned) || (r_halo && !is_device_ptr(r_halo)))
+    return fail(CPM_ERR_ARG, "cpm_part_ras_apply_local: vectors must be device memory");
   return ras_apply_device(ras, r_owned, z_owned, (cudaStream_t)stream, r_halo ? r_halo : R->hbuf);
 }
 
 int cpm_part_ras_apply(const cpm_ras* ras, const cpm_comm* comm, const double* r_owned,
                        double* z_owned, void* stream) {
   if (!ras || !r_owned || !z_owned) return fail(CPM_ERR_ARG, "cpm_part_ras_apply: null argument");
+  if (!is_device_ptr(r_owned) || !is_device_ptr(z_owned))
+    return fail(CPM_ERR_ARG, "cpm_part_ras_apply: vectors must be device memory");
   cudaStream_t s = (cudaStream_t)stream;
   CPM_TRY(ras_exchange(ras, comm, r_owned, s));
   return ras_apply_device(ras, r_owned, z_owned, s);

@@ -359,6 +359,10 @@ static __global__ void __launch_bounds__(TB) k_dcgs_dots(Seg S, int k, const dou
   const int64_t tfirst = (int64_t)lb * TB;
   for (int q = 0; q < ns - 1; ++q) issue(tfirst + q * stride, smp + (size_t)q * stage);
   double a1 = 0.0, a2 = 0.0;
+  // k > TB (only TB = 128 with GMRES(128): k = 129 at the cycle's last step): P = 1 and
+  // thread tid also owns column col2 = tid + TB (same element order as every column)
+  const int col2 = col + TB;
+  double b1 = 0.0, b2 = 0.0;
   int it = 0;
   for (int64_t t0 = tfirst; t0 < n; t0 += stride, ++it) {
     issue(t0 + (int64_t)(ns - 1) * stride, smp + (size_t)((it + ns - 1) % ns) * stage);
@@ -381,6 +385,18 @@ static __global__ void __launch_bounds__(TB) k_dcgs_dots(Seg S, int k, const dou
         a2 += cv.y * zv.y;
       }
     }
+    if (col2 < k) {  // P == 1 here
+      const double2* c = (const double2*)(sv + (size_t)col2 * SV + sub * R);
+      const double2* su = (const double2*)(sv + (size_t)(k - 1) * SV + sub * R);
+      const double2* sz = (const double2*)(sv + (size_t)k * SV + sub * R);
+      for (int m = 0; m < M / 2; ++m) {
+        const double2 cv = c[m], uv = su[m], zv = sz[m];
+        b1 += cv.x * uv.x;
+        b2 += cv.x * zv.x;
+        b1 += cv.y * uv.y;
+        b2 += cv.y * zv.y;
+      }
+    }
     __syncthreads();
   }
   cp_wait_all_v();
@@ -391,6 +407,10 @@ static __global__ void __launch_bounds__(TB) k_dcgs_dots(Seg S, int k, const dou
   if (sub == 0 && col < k) {
     partial[(size_t)blockIdx.x * pld + col] = a1;
     partial[(size_t)blockIdx.x * pld + k + col] = a2;
+  }
+  if (col2 < k) {
+    partial[(size_t)blockIdx.x * pld + col2] = b1;
+    partial[(size_t)blockIdx.x * pld + k + col2] = b2;
   }
   __threadfence();
   __syncthreads();
