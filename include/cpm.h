@@ -172,7 +172,8 @@ void cpm_ras_free(cpm_ras* ras);
  * [floor(r nA/R), floor((r+1) nA/R)) (reading R8); its local operator reads the
  * owned entries of a vector plus a HALO of other ranks' entries (the active nodes
  * in the stencil boxes of the tiles it evaluates).  Before every apply the halo
- * is exchanged with NCCL send/recv; every Krylov reduction is an NCCL allreduce.
+ * is exchanged with NCCL send/recv; every Krylov reduction is an NCCL allreduce
+ * (or, for a communicator from cpm_comm_init_host, the caller's host callbacks).
  * NCCL is loaded at run time (dlopen "libnccl.so.2"); without it the cpm_comm_*
  * calls return CPM_ERR_NCCL and the single-GPU API is unaffected. */
 typedef struct cpm_part cpm_part;
@@ -185,6 +186,25 @@ typedef struct cpm_part_info {
 /* 128-byte NCCL unique id (rank 0 creates it; broadcast it, e.g. with torch.distributed). */
 int cpm_comm_unique_id(void* id_out_128);
 int cpm_comm_init(const void* id_128, int rank, int nranks, cpm_comm** out);
+/* Host-staged transport (the second transport behind the same cpm_part_* calls):
+ * the two data-plane collectives of the partitioned path are delegated to caller
+ * callbacks on HOST buffers — used to run several ranks as processes sharing one
+ * GPU (NCCL refuses two ranks on one device), e.g. over a torch.distributed gloo
+ * group.  The library synchronises `stream`, copies the device data into pinned
+ * host staging, calls the callback, and copies the result back.
+ *   allreduce_sum(ctx, buf, n): buf[0..n) <- its sum over all ranks (in place).
+ *   alltoallv(ctx, send, send_counts, recv, recv_counts): send_counts[q] doubles
+ *     to rank q (blocks in rank order in `send`), recv_counts[q] doubles from
+ *     rank q (rank order in `recv`); counts have nranks entries, own entry 0.
+ * Callbacks return 0 on success; any other value fails the calling entry point
+ * with CPM_ERR_NCCL.  The struct is copied; ctx must outlive the communicator. */
+typedef struct cpm_host_transport {
+  void* ctx;
+  int (*allreduce_sum)(void* ctx, double* buf, int64_t n);
+  int (*alltoallv)(void* ctx, const double* send, const int64_t* send_counts, double* recv,
+                   const int64_t* recv_counts);
+} cpm_host_transport;
+int cpm_comm_init_host(const cpm_host_transport* transport, int rank, int nranks, cpm_comm** out);
 void cpm_comm_free(cpm_comm* comm);
 
 /* Build rank's partition of `band` (device work on stream).  Errors: CPM_ERR_ARG. */
@@ -272,6 +292,15 @@ typedef struct cpm_rd_params {
 } cpm_rd_params;
 int cpm_rd_step(const cpm_band* band, const cpm_rd_params* params, double* u, double* v,
                 cpm_solve_stats* su, cpm_solve_stats* sv, void* stream);
+
+/* cpm_part_rd_step — cpm_rd_step on this rank's owned slices of u and v (DEVICE
+ * arrays of n_owned doubles, updated in place): the reaction terms pointwise on the
+ * slice, then the two shifted solves by cpm_part_solve (halo exchanges and Krylov
+ * allreduces over comm; collective: every rank calls it).  Synchronises `stream`.
+ * Errors: those of cpm_rd_step and cpm_part_solve. */
+int cpm_part_rd_step(const cpm_part* part, const cpm_comm* comm, const cpm_rd_params* params,
+                     double* u_owned, double* v_owned, cpm_solve_stats* su, cpm_solve_stats* sv,
+                     void* stream);
 
 /* ---------------------------------------------------------------- profiling
  * When enabled, every kernel launched by the library on the caller's stream is

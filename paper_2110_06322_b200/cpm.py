@@ -70,6 +70,16 @@ class _RdParams(ctypes.Structure):
                 ("rtol", ctypes.c_double), ("restart", ctypes.c_int32), ("maxit", ctypes.c_int32)]
 
 
+_ALLRED_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.POINTER(ctypes.c_double), ctypes.c_int64)
+_ALLTOALLV_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.POINTER(ctypes.c_double),
+                                 ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_double),
+                                 ctypes.POINTER(ctypes.c_int64))
+
+
+class _HostTransport(ctypes.Structure):
+    _fields_ = [("ctx", ctypes.c_void_p), ("allreduce_sum", _ALLRED_FN), ("alltoallv", _ALLTOALLV_FN)]
+
+
 _vp = ctypes.c_void_p
 _SIGS = {
     "cpm_version": (ctypes.c_char_p, []),
@@ -97,6 +107,8 @@ _SIGS = {
     "cpm_kernel_launches": (ctypes.c_int64, []),
     "cpm_comm_unique_id": (ctypes.c_int, [_vp]),
     "cpm_comm_init": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, ctypes.POINTER(_vp)]),
+    "cpm_comm_init_host": (ctypes.c_int, [ctypes.POINTER(_HostTransport), ctypes.c_int, ctypes.c_int,
+                                          ctypes.POINTER(_vp)]),
     "cpm_comm_free": (None, [_vp]),
     "cpm_part_create": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, _vp, ctypes.POINTER(_vp)]),
     "cpm_part_get_info": (ctypes.c_int, [_vp, _vp]),
@@ -116,6 +128,8 @@ _SIGS = {
     "cpm_part_free": (None, [_vp]),
     "cpm_rd_step": (ctypes.c_int, [_vp, ctypes.POINTER(_RdParams), _vp, _vp, ctypes.POINTER(_SolveStats),
                                    ctypes.POINTER(_SolveStats), _vp]),
+    "cpm_part_rd_step": (ctypes.c_int, [_vp, _vp, ctypes.POINTER(_RdParams), _vp, _vp,
+                                        ctypes.POINTER(_SolveStats), ctypes.POINTER(_SolveStats), _vp]),
 }
 
 _lib = None
@@ -346,6 +360,21 @@ def cpm_rd_step(band: Band, u, v, a: float = 0.1, b: float = 0.9, gamma: float =
                             x.resid_true, x.bnorm, x.seconds) for x in (s1, s2))
 
 
+def cpm_part_rd_step(part, comm, u_owned, v_owned, a: float = 0.1, b: float = 0.9, gamma: float = 10.0,
+                     mu1: float = 1e-3, mu2: float = 1e-2, dt: float = 1e-3, rtol: float = 1e-10,
+                     restart: int = 50, maxit: int = 100000, stream=None):
+    """cpm_rd_step on this rank's owned slices (device tensors of n_owned, in place)."""
+    pu, su = _ptr_stream(u_owned, part.n_owned, True)
+    pv, _ = _ptr_stream(v_owned, part.n_owned, True)
+    prm = _RdParams(a, b, gamma, mu1, mu2, dt, rtol, restart, maxit)
+    s1, s2 = _SolveStats(), _SolveStats()
+    _check(load_library().cpm_part_rd_step(part.handle, comm.handle if comm else None, ctypes.byref(prm),
+                                           pu, pv, ctypes.byref(s1), ctypes.byref(s2), stream or su),
+           "cpm_part_rd_step")
+    return tuple(SolveStats(x.iterations, bool(x.converged), x.cycles, bool(x.breakdown), x.resid_est,
+                            x.resid_true, x.bnorm, x.seconds) for x in (s1, s2))
+
+
 def cpm_eval_sph(band: Band, l: int, m: int, scale: float, out, stream=None):
     po, so = _ptr_stream(out, band.n, True)
     _check(load_library().cpm_eval_sph(band.handle, int(l), int(m), float(scale), po, stream or so),
@@ -454,6 +483,48 @@ def cpm_comm_init(uid: bytes, rank: int, nranks: int) -> Comm:
     out = _vp()
     _check(load_library().cpm_comm_init(buf, int(rank), int(nranks), ctypes.byref(out)), "cpm_comm_init")
     return Comm(out)
+
+
+def cpm_comm_init_host(allreduce_sum, alltoallv, rank: int, nranks: int) -> Comm:
+    """Host-staged communicator (include/cpm.h cpm_comm_init_host).
+
+    allreduce_sum(buf: np.ndarray) sums buf over the ranks in place;
+    alltoallv(send, send_counts, recv, recv_counts) exchanges blocks in rank order
+    (numpy views of the library's pinned staging; counts are int64 arrays).
+    Both return None (an exception makes the library call fail)."""
+    nr = int(nranks)
+
+    def _ar(ctx, buf, n):
+        try:
+            allreduce_sum(np.ctypeslib.as_array(buf, shape=(int(n),)))
+            return 0
+        except Exception:  # pragma: no cover - reported through the library error
+            import traceback
+            traceback.print_exc()
+            return 1
+
+    def _a2a(ctx, send, sc, recv, rc):
+        try:
+            scn = np.ctypeslib.as_array(sc, shape=(nr,)).copy()
+            rcn = np.ctypeslib.as_array(rc, shape=(nr,)).copy()
+            ns, nrv = int(scn.sum()), int(rcn.sum())
+            sv = np.ctypeslib.as_array(send, shape=(ns,)) if ns else np.empty(0)
+            rv = np.ctypeslib.as_array(recv, shape=(nrv,)) if nrv else np.empty(0)
+            alltoallv(sv, scn, rv, rcn)
+            return 0
+        except Exception:  # pragma: no cover
+            import traceback
+            traceback.print_exc()
+            return 1
+
+    fa, fb = _ALLRED_FN(_ar), _ALLTOALLV_FN(_a2a)
+    tr = _HostTransport(None, fa, fb)
+    out = _vp()
+    _check(load_library().cpm_comm_init_host(ctypes.byref(tr), int(rank), nr, ctypes.byref(out)),
+           "cpm_comm_init_host")
+    c = Comm(out)
+    c._keep = (fa, fb, tr)  # the library holds the function pointers
+    return c
 
 
 def cpm_part_create(band: Band, rank: int, nranks: int, stream=None) -> Part:

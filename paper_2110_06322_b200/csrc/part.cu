@@ -79,8 +79,30 @@ int nccl_check(ncclResult_t r, const char* what) {
 }
 }  // namespace
 
+// pinned host staging of a host-transport communicator, at least n doubles
+static int host_stage(const cpm_comm* comm, size_t n) {
+  cpm_comm* c = const_cast<cpm_comm*>(comm);
+  if (c->cap >= n) return CPM_OK;
+  if (c->stage) cudaFreeHost(c->stage);
+  c->stage = nullptr;
+  c->cap = 0;
+  const size_t want = std::max<size_t>(n, 1024);
+  CPM_CUDA(cudaMallocHost(&c->stage, want * sizeof(double)));
+  c->cap = want;
+  return CPM_OK;
+}
+
 int comm_allreduce_sum(const cpm_comm* comm, double* buf, size_t n, cudaStream_t s) {
   if (!comm || comm->nranks == 1 || n == 0) return CPM_OK;
+  if (comm->host) {
+    CPM_TRY(host_stage(comm, n));
+    CPM_CUDA(cudaMemcpyAsync(comm->stage, buf, n * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CPM_CUDA(cudaStreamSynchronize(s));
+    if (comm->ht.allreduce_sum(comm->ht.ctx, comm->stage, (int64_t)n) != 0)
+      return fail(CPM_ERR_NCCL, "host transport: allreduce_sum callback failed");
+    CPM_CUDA(cudaMemcpyAsync(buf, comm->stage, n * sizeof(double), cudaMemcpyHostToDevice, s));
+    return CPM_OK;
+  }
   return nccl_check(g_nccl.AllReduce(buf, buf, n, ncclDouble, ncclSum, (ncclComm_t)comm->nccl, s),
                     "ncclAllReduce");
 }
@@ -389,6 +411,18 @@ int halo_exchange(const cpm_comm* comm, int rank, int nranks, const double* x, i
     k_gather_idx<<<g1(nSend), 256, 0, s>>>(nSend, sendidx, x, sendbuf);
     count_launch();
   }
+  if (comm->host) {  // host-staged: [send | recv] in pinned staging, the caller's alltoallv
+    const int64_t nRecv = recvOff[nranks];
+    CPM_TRY(host_stage(comm, (size_t)(nSend + nRecv)));
+    double* hs = comm->stage;
+    double* hr = comm->stage + nSend;
+    if (nSend > 0) CPM_CUDA(cudaMemcpyAsync(hs, sendbuf, nSend * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CPM_CUDA(cudaStreamSynchronize(s));
+    if (comm->ht.alltoallv(comm->ht.ctx, hs, sendCount.data(), hr, recvCount.data()) != 0)
+      return fail(CPM_ERR_NCCL, "host transport: alltoallv callback failed");
+    if (nRecv > 0) CPM_CUDA(cudaMemcpyAsync(recvbuf, hr, nRecv * sizeof(double), cudaMemcpyHostToDevice, s));
+    return CPM_OK;
+  }
   CPM_TRY(nccl_check(g_nccl.GroupStart(), "ncclGroupStart"));
   for (int q = 0; q < nranks; ++q) {
     if (q == rank) continue;
@@ -411,8 +445,12 @@ int part_exchange(const cpm_part* P, const cpm_comm* comm, const double* x, cuda
 
 }  // namespace cpm
 
+cpm_comm::~cpm_comm() {
+  if (stage) cudaFreeHost(stage);
+}
+
 cpm_part::~cpm_part() {
-  void* ps[] = {lb.tiles, lb.runs, lb.vb, lb.acell, halo, hbuf, sendidx, sendbuf};
+  void* ps[] = {lb.tiles, lb.runs, lb.vb, lb.acell, halo, hbuf, sendidx, sendbuf, rdstage};
   for (void* p : ps)
     if (p) cudaFree(p);
   lb.tiles = nullptr;
@@ -443,6 +481,18 @@ int cpm_comm_init(const void* id, int rank, int nranks, cpm_comm** out) {
   CPM_TRY(nccl_check(g_nccl.CommInitRank(&c, nranks, uid, rank), "ncclCommInitRank"));
   cpm_comm* cm = new cpm_comm();
   cm->nccl = c;
+  cm->rank = rank;
+  cm->nranks = nranks;
+  *out = cm;
+  return CPM_OK;
+}
+
+int cpm_comm_init_host(const cpm_host_transport* tr, int rank, int nranks, cpm_comm** out) {
+  if (!tr || !out || !tr->allreduce_sum || !tr->alltoallv || nranks < 1 || rank < 0 || rank >= nranks)
+    return fail(CPM_ERR_ARG, "cpm_comm_init_host: bad arguments");
+  cpm_comm* cm = new cpm_comm();
+  cm->host = true;
+  cm->ht = *tr;
   cm->rank = rank;
   cm->nranks = nranks;
   *out = cm;
@@ -503,6 +553,10 @@ int cpm_part_apply(const cpm_part* p, const cpm_comm* comm, double c, const doub
   return apply_device_split(&p->lb, c, u_owned, p->hbuf, y_owned, nullptr, 0, s);
 }
 
+static int part_solve(const cpm_part* p, const cpm_comm* comm, double c, const double* f_owned,
+                      double* u_owned, double rtol, int restart, int maxit, const cpm_ras* ras,
+                      cpm_solve_stats* stats, void* stream);
+
 int cpm_part_solve(const cpm_part* p, const cpm_comm* comm, double c, const double* f_owned,
                    double* u_owned, double rtol, int restart, int maxit, const cpm_ras* ras,
                    cpm_solve_stats* stats, void* stream) {
@@ -510,6 +564,36 @@ int cpm_part_solve(const cpm_part* p, const cpm_comm* comm, double c, const doub
   if (!is_device_ptr(f_owned) || !is_device_ptr(u_owned))
     return fail(CPM_ERR_ARG, "cpm_part_solve: vectors must be device memory");
   if (p->nranks > 1 && !comm) return fail(CPM_ERR_ARG, "cpm_part_solve: needs a communicator");
+  return part_solve(p, comm, c, f_owned, u_owned, rtol, restart, maxit, ras, stats, stream);
+}
+
+int cpm_part_rd_step(const cpm_part* p, const cpm_comm* comm, const cpm_rd_params* prm, double* u_owned,
+                     double* v_owned, cpm_solve_stats* su, cpm_solve_stats* sv, void* stream) {
+  if (!p || !prm || !u_owned || !v_owned) return fail(CPM_ERR_ARG, "cpm_part_rd_step: null argument");
+  if (u_owned == v_owned) return fail(CPM_ERR_ARG, "cpm_part_rd_step: u and v must not alias");
+  if (!(prm->dt > 0.0) || !(prm->mu1 > 0.0) || !(prm->mu2 > 0.0))
+    return fail(CPM_ERR_ARG, "cpm_part_rd_step: dt, mu1, mu2 must be > 0");
+  if (!is_device_ptr(u_owned) || !is_device_ptr(v_owned))
+    return fail(CPM_ERR_ARG, "cpm_part_rd_step: vectors must be device memory");
+  if (p->nranks > 1 && !comm) return fail(CPM_ERR_ARG, "cpm_part_rd_step: needs a communicator");
+  cudaStream_t s = (cudaStream_t)stream;
+  cpm_part* mp = const_cast<cpm_part*>(p);
+  if (!mp->rdstage) CPM_CUDA(cudaMalloc(&mp->rdstage, sizeof(double) * 2 * std::max<int64_t>(p->nOwned, 1)));
+  double* ru = mp->rdstage;
+  double* rv = mp->rdstage + std::max<int64_t>(p->nOwned, 1);
+  const double c1 = 1.0 / (prm->dt * prm->mu1), c2 = 1.0 / (prm->dt * prm->mu2);
+  // the reaction terms on the owned slice (pointwise: no exchange), then two shifted
+  // partitioned solves warm-started from the old state (reading R14)
+  CPM_TRY(rd_rhs_device(p->nOwned, u_owned, v_owned, prm, c1, c2, ru, rv, s));
+  cpm_solve_stats l1, l2;
+  CPM_TRY(part_solve(p, comm, c1, ru, u_owned, prm->rtol, prm->restart, prm->maxit, nullptr, su ? su : &l1, s));
+  CPM_TRY(part_solve(p, comm, c2, rv, v_owned, prm->rtol, prm->restart, prm->maxit, nullptr, sv ? sv : &l2, s));
+  return CPM_OK;
+}
+
+static int part_solve(const cpm_part* p, const cpm_comm* comm, double c, const double* f_owned,
+                      double* u_owned, double rtol, int restart, int maxit, const cpm_ras* ras,
+                      cpm_solve_stats* stats, void* stream) {
   PrecOp M;
   if (ras) {
     cpm_ras_info ri;

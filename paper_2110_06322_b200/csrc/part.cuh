@@ -6,8 +6,13 @@
 #include "krylov.cuh"
 
 struct cpm_comm {
-  void* nccl = nullptr;  // ncclComm_t
+  void* nccl = nullptr;  // ncclComm_t (NCCL transport)
   int rank = 0, nranks = 1;
+  bool host = false;     // host-staged transport (cpm_comm_init_host)
+  cpm_host_transport ht{};
+  double* stage = nullptr;  // pinned host staging: [send | recv] or the allreduce buffer
+  size_t cap = 0;           // doubles
+  ~cpm_comm();
 };
 
 struct cpm_part {
@@ -22,10 +27,13 @@ struct cpm_part {
   double* sendbuf = nullptr;
   std::vector<int64_t> sendCount, sendOff, recvCount, recvOff;
   cpm::Workspace* ws = nullptr;
+  double* rdstage = nullptr;                   // 2 * nOwned: right-hand sides of cpm_part_rd_step
   ~cpm_part();
 };
 
 namespace cpm {
+int rd_rhs_device(int64_t n, const double* u, const double* v, const cpm_rd_params* p, double c1,
+                  double c2, double* ru, double* rv, cudaStream_t s);
 int comm_allreduce_sum(const cpm_comm* comm, double* buf, size_t n, cudaStream_t s);
 int part_exchange(const cpm_part* P, const cpm_comm* comm, const double* x, cudaStream_t s);
 int halo_exchange(const cpm_comm* comm, int rank, int nranks, const double* x, int64_t nSend,

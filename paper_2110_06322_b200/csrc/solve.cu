@@ -74,6 +74,19 @@ __global__ void k_rd_rhs(int64_t n, const double* __restrict__ u, const double* 
 }
 }  // namespace
 
+namespace cpm {
+// ru, rv (device, n each) = the two right-hand sides of an IMEX step (reading R14)
+int rd_rhs_device(int64_t n, const double* u, const double* v, const cpm_rd_params* p, double c1,
+                  double c2, double* ru, double* rv, cudaStream_t s) {
+  ProfScope ps(K_AXPY, s);
+  const int grid = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
+  k_rd_rhs<<<std::max(grid, 1), 256, 0, s>>>(n, u, v, p->a, p->b, p->gamma, p->dt, c1, c2, ru, rv);
+  count_launch();
+  CPM_CUDA(cudaGetLastError());
+  return CPM_OK;
+}
+}  // namespace cpm
+
 extern "C" int cpm_rd_step(const cpm_band* b, const cpm_rd_params* p, double* u, double* v,
                            cpm_solve_stats* su, cpm_solve_stats* sv, void* stream) {
   if (!b || !p || !u || !v) return fail(CPM_ERR_ARG, "cpm_rd_step: null argument");
@@ -89,14 +102,7 @@ extern "C" int cpm_rd_step(const cpm_band* b, const cpm_rd_params* p, double* u,
     CPM_CUDA(cudaMalloc(&mb->dstage1, sizeof(double) * std::max<int64_t>(b->nA, 1)));
   }
   const double c1 = 1.0 / (p->dt * p->mu1), c2 = 1.0 / (p->dt * p->mu2);
-  {
-    ProfScope ps(K_AXPY, s);
-    const int grid = (int)std::min<int64_t>((b->nA + 255) / 256, 148 * 8);
-    k_rd_rhs<<<std::max(grid, 1), 256, 0, s>>>(b->nA, u, v, p->a, p->b, p->gamma, p->dt, c1, c2,
-                                               mb->dstage0, mb->dstage1);
-    count_launch();
-    CPM_CUDA(cudaGetLastError());
-  }
+  CPM_TRY(rd_rhs_device(b->nA, u, v, p, c1, c2, mb->dstage0, mb->dstage1, s));
   cpm_solve_stats l1, l2;
   for (int q = 0; q < 2; ++q) {
     const double c = q == 0 ? c1 : c2;

@@ -573,6 +573,103 @@ static __global__ void __launch_bounds__(256) k_dcgs_dots_bulk(Seg S, int k, con
   epi(s);
 }
 
+// ---- register-direct variant of the reduction pass: every basis column is read
+// ONCE from HBM straight into registers (coalesced 16-byte loads, no shared-memory
+// staging).  Warp w of the block owns the columns i = w, w + 8, ... (< k) and keeps
+// their two partial dots <Q_i, u_j>, <Q_i, z> per lane; a tile is 128 consecutive
+// elements, lane l taking elements 2l, 2l+1, 64+2l, 65+2l; every warp also reads the
+// tile's u_j and z (L1 hits after the first warp).  Fixed association order: per
+// lane the tiles in order, then the warp shuffle tree, then the blocks in index
+// order (the last block of the segment, as k_dcgs_dots).  KW = max columns per warp.
+template <int KW, class Epi = NoEpi>
+static __global__ void __launch_bounds__(256, 2) k_dcgs_dots_direct(
+    Seg S, int k, const double* __restrict__ V, int64_t ldv, const double* __restrict__ z, double* partial,
+    int pld, double* out, int ldo, unsigned* counters, const int* __restrict__ skip, Epi epi = Epi()) {
+  constexpr int TB = 256, NW = TB / 32, TE = 128;
+  pdl_wait();
+  if (skip && *skip) return;
+  __shared__ bool last;
+  const int s = blockIdx.x / S.gps, lb = blockIdx.x % S.gps;
+  const int64_t o0 = S.off[s], n = S.off[s + 1] - o0;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const double* uj = V + (size_t)(k - 1) * ldv + o0;  // the lagged vector is the last column
+  const double* zz = z + o0;
+  double a1[KW], a2[KW];
+#pragma unroll
+  for (int c = 0; c < KW; ++c) a1[c] = a2[c] = 0.0;
+  const bool vec2 = ((o0 | ldv) & 1) == 0;  // 16-byte aligned columns
+  const int64_t stride = (int64_t)S.gps * TE;
+  for (int64_t t0 = (int64_t)lb * TE; t0 < n; t0 += stride) {
+    const int64_t e0 = t0 + 2 * lane, e1 = t0 + 64 + 2 * lane;
+    double u0, u1, u2, u3, z0, z1, z2, z3;
+    const bool full = t0 + TE <= n;
+    if (full && vec2) {
+      const double2 ua = __ldg((const double2*)(uj + e0)), ub = __ldg((const double2*)(uj + e1));
+      const double2 za = __ldg((const double2*)(zz + e0)), zb = __ldg((const double2*)(zz + e1));
+      u0 = ua.x; u1 = ua.y; u2 = ub.x; u3 = ub.y;
+      z0 = za.x; z1 = za.y; z2 = zb.x; z3 = zb.y;
+    } else {
+      u0 = e0 < n ? __ldg(uj + e0) : 0.0; u1 = e0 + 1 < n ? __ldg(uj + e0 + 1) : 0.0;
+      u2 = e1 < n ? __ldg(uj + e1) : 0.0; u3 = e1 + 1 < n ? __ldg(uj + e1 + 1) : 0.0;
+      z0 = e0 < n ? __ldg(zz + e0) : 0.0; z1 = e0 + 1 < n ? __ldg(zz + e0 + 1) : 0.0;
+      z2 = e1 < n ? __ldg(zz + e1) : 0.0; z3 = e1 + 1 < n ? __ldg(zz + e1 + 1) : 0.0;
+    }
+#pragma unroll
+    for (int c = 0; c < KW; ++c) {
+      const int i = warp + c * NW;
+      if (i < k) {
+        const double* col = V + (size_t)i * ldv + o0;
+        double v0, v1, v2, v3;
+        if (full && vec2) {
+          const double2 va = __ldcs((const double2*)(col + e0)), vb = __ldcs((const double2*)(col + e1));
+          v0 = va.x; v1 = va.y; v2 = vb.x; v3 = vb.y;
+        } else {
+          v0 = e0 < n ? __ldcs(col + e0) : 0.0; v1 = e0 + 1 < n ? __ldcs(col + e0 + 1) : 0.0;
+          v2 = e1 < n ? __ldcs(col + e1) : 0.0; v3 = e1 + 1 < n ? __ldcs(col + e1 + 1) : 0.0;
+        }
+        a1[c] = fma(v0, u0, a1[c]); a2[c] = fma(v0, z0, a2[c]);
+        a1[c] = fma(v1, u1, a1[c]); a2[c] = fma(v1, z1, a2[c]);
+        a1[c] = fma(v2, u2, a1[c]); a2[c] = fma(v2, z2, a2[c]);
+        a1[c] = fma(v3, u3, a1[c]); a2[c] = fma(v3, z3, a2[c]);
+      }
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < KW; ++c) {
+    const int i = warp + c * NW;
+    if (i < k) {
+      const double r1 = warp_sum(a1[c]), r2 = warp_sum(a2[c]);
+      if (lane == 0) {
+        partial[(size_t)blockIdx.x * pld + i] = r1;
+        partial[(size_t)blockIdx.x * pld + k + i] = r2;
+      }
+    }
+  }
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) last = (atomicAdd(counters + s, 1u) == (unsigned)S.gps - 1u);
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  for (int i = warp; i < 2 * k; i += 2 * NW) {
+    const int i2 = i + NW;
+    if (i2 < 2 * k) {
+      double a, a2v;
+      partial_sum2(partial, (size_t)s * S.gps, pld, S.gps, i, i2, lane, a, a2v);
+      if (lane == 0) {
+        out[(size_t)s * ldo + i] = a;
+        out[(size_t)s * ldo + i2] = a2v;
+      }
+    } else {
+      const double a = partial_sum(partial, (size_t)s * S.gps, pld, S.gps, i, lane);
+      if (lane == 0) out[(size_t)s * ldo + i] = a;
+    }
+  }
+  if (tid == 0) counters[s] = 0u;
+  __syncthreads();
+  epi(s);
+}
+
 template <int TB>
 static __global__ void __launch_bounds__(TB) k_dcgs_update(Seg S, int k, double* V, int64_t ldv,
                                                            const double* __restrict__ z,
@@ -850,7 +947,17 @@ inline int launch_dcgs_dots_epi(const vec::Seg& S, int k, const double* V, int64
     const char* v = getenv("CPM_DOTS_BULK");
     return !v || *v != '0';
   }();
-  if (bulk && k <= 52) {  // a stage of (k+1) 2 KB columns: two blocks per SM
+  static const bool direct = [] {  // CPM_DOTS_DIRECT=0: the staged kernels (A/B)
+    const char* v = getenv("CPM_DOTS_DIRECT");
+    return !v || *v != '0';
+  }();
+  if (direct && k <= 8 * 8) {
+    CPM_CUDA(launch_pdl(vec::k_dcgs_dots_direct<8, Epi>, dim3(grid), dim3(256), 0, st, S, k, V, ldv, z, partial,
+                        pld, out, ldo, counters, skip, epi));
+  } else if (direct && k <= 8 * 17) {
+    CPM_CUDA(launch_pdl(vec::k_dcgs_dots_direct<17, Epi>, dim3(grid), dim3(256), 0, st, S, k, V, ldv, z, partial,
+                        pld, out, ldo, counters, skip, epi));
+  } else if (bulk && k <= 52) {  // a stage of (k+1) 2 KB columns: two blocks per SM
     const size_t stage = (size_t)(k + 1) * (256 + 4) * sizeof(double);
     const int ns = depth(stage);
     static bool attrb = false;

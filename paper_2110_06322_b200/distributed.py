@@ -69,10 +69,32 @@ def broadcast_uid(uid: bytes | None, group=None) -> bytes:
     return bytes(t.cpu().numpy().tobytes())
 
 
-class DistributedCPM:
-    """This rank's slab of a band, its NCCL communicator and the distributed ops."""
+def host_transport_fns(group=None):
+    """(allreduce_sum, alltoallv) over a torch.distributed group on host tensors (gloo):
+    the callbacks of cpm_comm_init_host (include/cpm.h)."""
+    import torch
+    import torch.distributed as dist
 
-    def __init__(self, band, group=None):
+    def allreduce_sum(buf):
+        t = torch.from_numpy(buf)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+
+    def alltoallv(send, send_counts, recv, recv_counts):
+        dist.all_to_all_single(torch.from_numpy(recv), torch.from_numpy(send),
+                               output_split_sizes=[int(c) for c in recv_counts],
+                               input_split_sizes=[int(c) for c in send_counts], group=group)
+
+    return allreduce_sum, alltoallv
+
+
+class DistributedCPM:
+    """This rank's slab of a band, its communicator and the distributed ops.
+
+    transport="nccl": NCCL inside libcpm.so (one GPU per rank); transport="host": the
+    host-staged transport over `group` (gloo), which runs several ranks as processes
+    sharing one GPU."""
+
+    def __init__(self, band, group=None, transport="nccl"):
         import torch.distributed as dist
 
         from . import cpm
@@ -86,9 +108,15 @@ class DistributedCPM:
         halo = cpm.cpm_part_halo_nodes(self.part)
         send, counts = exchange_requests(halo, bounds, group)
         cpm.cpm_part_set_send(self.part, send, counts)
-        uid = cpm.cpm_comm_unique_id() if self.rank == 0 else None
-        uid = broadcast_uid(uid, group)
-        self.comm = cpm.cpm_comm_init(uid, self.rank, self.nranks)
+        if transport == "host":
+            ar, a2a = host_transport_fns(group)
+            self.comm = cpm.cpm_comm_init_host(ar, a2a, self.rank, self.nranks)
+        elif transport == "nccl":
+            uid = cpm.cpm_comm_unique_id() if self.rank == 0 else None
+            uid = broadcast_uid(uid, group)
+            self.comm = cpm.cpm_comm_init(uid, self.rank, self.nranks)
+        else:
+            raise ValueError(f"unknown transport {transport!r}")
 
     @property
     def lo(self):
@@ -113,6 +141,12 @@ class DistributedCPM:
         send, counts = exchange_requests(halo, slab_bounds(self.band.n, self.nranks), group)
         cpm.cpm_ras_set_send(ras, send, counts)
         return ras
+
+    def rd_step(self, u_owned, v_owned, **params):
+        """One partitioned Schnakenberg IMEX step (cpm_part_rd_step) on the owned slices."""
+        from . import cpm
+
+        return cpm.cpm_part_rd_step(self.part, self.comm, u_owned, v_owned, **params)
 
     def solve(self, c, f_owned, u_owned, rtol=1e-10, restart=50, maxit=100000, ras=None):
         from . import cpm

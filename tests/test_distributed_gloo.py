@@ -78,3 +78,54 @@ def test_slab_bounds_match_oracle():
 
     for n, R in [(10, 3), (4146590, 8), (7, 7)]:
         assert slab_bounds(n, R).tolist() == osb(n, R)
+
+
+def _transport_worker(rank, world, port, q):
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2110_06322_b200.distributed import host_transport_fns
+
+        ar, a2a = host_transport_fns()
+        buf = np.arange(5, dtype=np.float64) * (rank + 1)
+        ar(buf)
+        # rank r sends (r + 1) * 10 + q, repeated q + 1 times, to rank q != r
+        sc = np.array([0 if q_ == rank else q_ + 1 for q_ in range(world)], dtype=np.int64)
+        rc = np.array([0 if q_ == rank else rank + 1 for q_ in range(world)], dtype=np.int64)
+        send = np.concatenate([np.full(sc[q_], (rank + 1) * 10.0 + q_) for q_ in range(world)])
+        recv = np.empty(int(rc.sum()))
+        a2a(send, sc, recv, rc)
+        q.put((rank, buf.tolist(), recv.tolist()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_host_transport_callbacks_gloo(world):
+    """The callbacks behind cpm_comm_init_host (distributed.host_transport_fns):
+    in-place sum over the ranks, and the rank-ordered alltoallv blocks."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_transport_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(world):
+        r, buf, recv = q.get(timeout=120)
+        res[r] = (buf, recv)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    tot = sum(r + 1 for r in range(world))
+    for r in range(world):
+        buf, recv = res[r]
+        assert buf == [float(i * tot) for i in range(5)]
+        want = []
+        for src in range(world):
+            if src != r:
+                want += [(src + 1) * 10.0 + r] * (r + 1)
+        assert recv == want

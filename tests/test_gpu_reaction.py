@@ -63,3 +63,22 @@ def test_rd_step_errors(cpm):
         cpm.cpm_rd_step(gb, u, v, dt=0.0)
     with pytest.raises(cpm.CpmError, match="device"):
         cpm.cpm_rd_step(gb, u.cpu().numpy(), v)
+
+
+def test_part_rd_step_single_rank_equals_rd_step(cpm):
+    """cpm_part_rd_step with one rank (no communicator) is cpm_rd_step, bit for bit."""
+    from paper_2110_06322_b200 import cpm as C
+
+    gb = cpm.cpm_build_band("sphere", 0.1)
+    ob = OBand(Sphere(1.0), 0.1)
+    ga = cpm.cpm_band_active_coords(gb).astype(np.int64)
+    p = SchnakenbergParams()
+    ug, vg = initial_state(ob, p, ijk=ga)
+    u1, v1 = torch.from_numpy(ug).cuda(), torch.from_numpy(vg).cuda()
+    u2, v2 = u1.clone(), v1.clone()
+    part = C.cpm_part_create(gb, 0, 1)
+    for _ in range(2):
+        a1, b1 = cpm.cpm_rd_step(gb, u1, v1)
+        a2, b2 = C.cpm_part_rd_step(part, None, u2, v2)
+        assert (a1.iterations, b1.iterations) == (a2.iterations, b2.iterations)
+    assert torch.equal(u1, u2) and torch.equal(v1, v2)
