@@ -692,6 +692,7 @@ def run_partitioned(args):
                                       + ("(host-staged gloo transport, ranks sharing a GPU: NOT a scaling number)"
                                          if host else "(NCCL halo send/recv + allreduce)"),
                        "rank0_owned": hi - lo, "rank0_halo": pinfo.n_halo, "rank0_tiles": nT_local,
+                       "rank0_interior_tiles": pinfo.n_interior_tiles,
                        "l2": "inputs larger than L2 at N <= 4; the timed applies include the halo exchange"},
             "solve": {"seconds_median": solve_ms / 1e3, "iterations": st.iterations, "converged": st.converged,
                       "resid_true_rel": st.resid_true / st.bnorm, "kind": "partitioned GMRES(50) (NCCL allreduce)"},

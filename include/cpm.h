@@ -181,6 +181,8 @@ typedef struct cpm_part_info {
   int32_t rank, nranks;
   int64_t lo, hi;        /* owned band-order range [lo, hi) */
   int64_t n_owned, n_halo, n_tiles, n_send;
+  int64_t n_interior_tiles; /* tiles [0, n_interior_tiles) read no halo node: their extend
+                               overlaps the halo exchange */
 } cpm_part_info;
 
 /* 128-byte NCCL unique id (rank 0 creates it; broadcast it, e.g. with torch.distributed). */

@@ -418,7 +418,7 @@ def cpm_version() -> str:
 class _PartInfo(ctypes.Structure):
     _fields_ = [("rank", ctypes.c_int32), ("nranks", ctypes.c_int32), ("lo", ctypes.c_int64),
                 ("hi", ctypes.c_int64), ("n_owned", ctypes.c_int64), ("n_halo", ctypes.c_int64),
-                ("n_tiles", ctypes.c_int64), ("n_send", ctypes.c_int64)]
+                ("n_tiles", ctypes.c_int64), ("n_send", ctypes.c_int64), ("n_interior_tiles", ctypes.c_int64)]
 
 
 class Part:
@@ -435,6 +435,7 @@ class Part:
         self.rank, self.nranks = inf.rank, inf.nranks
         self.lo, self.hi = inf.lo, inf.hi
         self.n_owned, self.n_halo, self.n_tiles, self.n_send = inf.n_owned, inf.n_halo, inf.n_tiles, inf.n_send
+        self.n_interior_tiles = inf.n_interior_tiles
 
     @property
     def handle(self):

@@ -147,13 +147,13 @@ __global__ void __launch_bounds__(kNtThreads, 8)
                 const double* __restrict__ uh, uint32_t split, const double* __restrict__ tx,
                 const double* __restrict__ ty, const double* __restrict__ tz,
                 const uint32_t* __restrict__ eoff, double* __restrict__ vb,
-                const int* __restrict__ skip, int pfd) {
+                const int* __restrict__ skip, int pfd, int tbase, int tend) {
   // The band metadata (header, node offsets, run descriptors) is constant: it is
   // requested before pdl_wait(); u is read and vb written only after it.
   extern __shared__ double smn[];
   double* box = smn;
   uint64_t* desc = (uint64_t*)(box + boxCells);
-  const int t = blockIdx.x, tid = threadIdx.x;
+  const int t = tbase + (int)blockIdx.x, tid = threadIdx.x;  // tiles [tbase, tend)
   const TileHdr* T = tiles + t;
   const int e0 = T->e0, ne = T->e1 - e0, r0 = T->r0, r1 = T->r1;
   const int np2 = 2 * T->np, nslot = 2 * ne - np2;
@@ -209,7 +209,7 @@ __global__ void __launch_bounds__(kNtThreads, 8)
   // The tile a CTA about one residency wave later will take (t + pfd): its
   // descriptors and node offsets into L2 now, so that CTA's dependent loads are
   // L2 hits (one lane; the header load it needs is itself that CTA's first load).
-  if (tid == kNtThreads - 32 && t + pfd < (int)gridDim.x) {
+  if (tid == kNtThreads - 32 && t + pfd < tend) {
     const TileHdr* F = tiles + t + pfd;
     const int f0 = F->e0, f1 = F->e1, q0 = F->r0, q1 = F->r1;
     prefetch_l2_bytes(runs + q0, (size_t)(q1 - q0) * 8);
@@ -218,7 +218,7 @@ __global__ void __launch_bounds__(kNtThreads, 8)
     prefetch_l2_bytes(tz + f0, (size_t)(f1 - f0) * 8);
     prefetch_l2_bytes(eoff + f0, (size_t)(f1 - f0) * 4);
     // and the header that lane will read one wave later
-    if (t + 2 * pfd < (int)gridDim.x) prefetch_l2_bytes(tiles + t + 2 * pfd, sizeof(TileHdr));
+    if (t + 2 * pfd < tend) prefetch_l2_bytes(tiles + t + 2 * pfd, sizeof(TileHdr));
   }
   cp_wait<0>();
   __syncthreads();
@@ -338,13 +338,10 @@ int apply_device(const cpm_band* b, double c, const double* u, double* y, const 
   return apply_device_split(b, c, u, u, y, scale, lds, s, skip);
 }
 
-int apply_device_split(const cpm_band* b, double c, const double* u, const double* uh, double* y,
-                       const double* scale, int lds, cudaStream_t s, const int* skip) {
-  if (b->nT == 0) return CPM_OK;  // no tiles (an empty sub-band): nothing to write
-  const double ih2 = 1.0 / (b->h * b->h);
-  const double diag = c + 6.0 * ih2;
-  // L2 prefetch distance in tiles (both kernels): one wave of resident extend CTAs,
-  // 8 per SM (measured: 0.5x and 2x are slower; CPM_EXT_PFD / CPM_LAP_PFD override)
+namespace {
+// L2 prefetch distance in tiles (both kernels): one wave of resident extend CTAs,
+// 8 per SM (measured: 0.5x and 2x are slower; CPM_EXT_PFD / CPM_LAP_PFD override)
+int prefetch_distance() {
   static const int pfd = [] {
     const char* v = getenv("CPM_EXT_PFD");
     if (v) return atoi(v);
@@ -353,10 +350,17 @@ int apply_device_split(const cpm_band* b, double c, const double* u, const doubl
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     return 8 * sms;
   }();
-  {
-    const int descCap = 512;
-    const size_t smem = (size_t)b->maxBox * 8 + (size_t)descCap * 8;
-    ProfScope ps(K_EXTEND, s);
+  return pfd;
+}
+}  // namespace
+
+int extend_tiles(const cpm_band* b, const double* u, const double* uh, cudaStream_t s, const int* skip,
+                 int t0, int t1) {
+  if (t1 <= t0) return CPM_OK;
+  const int pfd = prefetch_distance();
+  const int descCap = 512;
+  const size_t smem = (size_t)b->maxBox * 8 + (size_t)descCap * 8;
+  ProfScope ps(K_EXTEND, s);
 #define CPM_EXTNT(Z)                                                                         \
   do {                                                                                       \
     static bool attr = false;                                                                \
@@ -365,26 +369,38 @@ int apply_device_split(const cpm_band* b, double c, const double* u, const doubl
                                     227 * 1024));                                            \
       attr = true;                                                                           \
     }                                                                                        \
-    CPM_CUDA(launch_pdl(k_extend_nt<Z>, dim3((unsigned)b->nT), dim3(kNtThreads), smem, s,       \
+    CPM_CUDA(launch_pdl(k_extend_nt<Z>, dim3((unsigned)(t1 - t0)), dim3(kNtThreads), smem, s,  \
                         b->tiles, (int)b->maxBox, descCap, (const uint64_t*)b->runs, u, uh,     \
                         (uint32_t)b->srcSplit, (const double*)b->tx, (const double*)b->ty,      \
-                        (const double*)b->tz, (const uint32_t*)b->eoff, b->vb, skip, pfd));     \
+                        (const double*)b->tz, (const uint32_t*)b->eoff, b->vb, skip, pfd, t0, t1)); \
   } while (0)
-    if (b->zeroFill) CPM_EXTNT(true); else CPM_EXTNT(false);
+  if (b->zeroFill) CPM_EXTNT(true); else CPM_EXTNT(false);
 #undef CPM_EXTNT
-    count_launch();
-  }
-  {
-    ProfScope ps(K_LAPLACE, s);
-    // 128 threads per tile: 16 resident tiles per SM keep enough loads in flight
-    static const int pfd2 = getenv("CPM_LAP_PFD") ? atoi(getenv("CPM_LAP_PFD")) : pfd;
-    CPM_CUDA(launch_pdl(k_laplace<128>, dim3((unsigned)b->nT), dim3(128), 0, s, b->tiles, u,
-                        (const uint16_t*)b->acell, (const double*)b->vb, y, diag, ih2, scale, lds,
-                        skip, pfd2));
-    count_launch();
-  }
+  count_launch();
   CPM_CUDA(cudaGetLastError());
   return CPM_OK;
+}
+
+int laplace_tiles(const cpm_band* b, double c, const double* u, double* y, const double* scale, int lds,
+                  cudaStream_t s, const int* skip) {
+  const double ih2 = 1.0 / (b->h * b->h);
+  const double diag = c + 6.0 * ih2;
+  ProfScope ps(K_LAPLACE, s);
+  // 128 threads per tile: 16 resident tiles per SM keep enough loads in flight
+  static const int pfd2 = getenv("CPM_LAP_PFD") ? atoi(getenv("CPM_LAP_PFD")) : prefetch_distance();
+  CPM_CUDA(launch_pdl(k_laplace<128>, dim3((unsigned)b->nT), dim3(128), 0, s, b->tiles, u,
+                      (const uint16_t*)b->acell, (const double*)b->vb, y, diag, ih2, scale, lds,
+                      skip, pfd2));
+  count_launch();
+  CPM_CUDA(cudaGetLastError());
+  return CPM_OK;
+}
+
+int apply_device_split(const cpm_band* b, double c, const double* u, const double* uh, double* y,
+                       const double* scale, int lds, cudaStream_t s, const int* skip) {
+  if (b->nT == 0) return CPM_OK;  // no tiles (an empty sub-band): nothing to write
+  CPM_TRY(extend_tiles(b, u, uh, s, skip, 0, b->nT));
+  return laplace_tiles(b, c, u, y, scale, lds, s, skip);
 }
 
 }  // namespace cpm

@@ -119,6 +119,7 @@ struct cpm_band {
   int M = 0;
   int64_t nA = 0, nG = 0, nE = 0;  // active, ghost, eval (= nA + nG for a full band)
   int nT = 0;                      // tiles
+  int nTint = 0;                   // partitioned sub-bands: tiles [0, nTint) read no halo source
   int64_t nRuns = 0;
   int maxBox = 0;
   bool zeroFill = false;
@@ -160,6 +161,12 @@ int apply_device(const cpm_band* b, double c, const double* u, double* y, const 
 // as apply_device, with fill-run sources >= b->srcSplit read from uh[src - srcSplit]
 int apply_device_split(const cpm_band* b, double c, const double* u, const double* uh, double* y,
                        const double* scale, int lds, cudaStream_t s, const int* skip = nullptr);
+// The two halves of apply_device_split, for the overlapped partitioned apply
+// (part.cu): the extend of tiles [t0, t1) (E u into vb), and the laplace of all tiles.
+int extend_tiles(const cpm_band* b, const double* u, const double* uh, cudaStream_t s, const int* skip,
+                 int t0, int t1);
+int laplace_tiles(const cpm_band* b, double c, const double* u, double* y, const double* scale, int lds,
+                  cudaStream_t s, const int* skip);
 // build.cu
 int build_band(const cpm_surface* surf, double h, int p, double L, cudaStream_t s, cpm_band** out);
 void free_band(cpm_band* b);

@@ -6,17 +6,24 @@
 // iteration count is the number of Arnoldi steps, right preconditioning in the
 // flexible form (Z_j = M v_j stored).
 //
-// Device-resident design:
-//  * The basis is stored UNNORMALISED, V_i = w_i, with sc_i = 1/||w_i|| kept
-//    on the device; every kernel applies sc_i on the fly, so no normalisation
-//    pass exists (one HBM pass per Arnoldi step saved).
-//  * One Arnoldi step = apply (2 kernels) + 3 fused passes over the basis:
-//      mdot        h1 = V^T w
-//      cgs_update  w <- w - V h1  AND  h2 = V^T w   (same sweep, sub-chunk in smem)
-//      cgs_final   V_{j+1} <- w - V h2  AND  ||V_{j+1}||^2
-//    followed by a one-thread Hessenberg/Givens kernel.  Reductions are
-//    deterministic: per-block partials in a fixed sub-chunk assignment, summed
-//    in block order by the last block to finish (threadfence + counter).
+// Device-resident design (DESIGN.md §Krylov design):
+//  * Unpreconditioned GMRES (one GPU, and partitioned over ranks) uses DELAYED CGS2
+//    (reading R15): per Arnoldi step the operator apply (extend + laplace) and TWO
+//    passes over the basis — the reduction pass (Q^T u_j, u_j.u_j, Q^T z, u_j.z;
+//    vecops.cuh k_dcgs_dots*) and the update pass (q_j and the next lagged vector
+//    u_{j+1} in one read of Q; k_dcgs_update*).  The Hessenberg column, the Givens
+//    rotation, the convergence test and the update coefficients are formed by the
+//    step body (dcgs_step_body): on one GPU as the epilogue of the block that
+//    completes the reduction, with several ranks by k_dcgs_step after the allreduce.
+//  * FGMRES (right-preconditioned by RAS; Z_j = M q_j stored) keeps CGS2 with an
+//    UNNORMALISED basis (sc_i = 1/||w_i|| on the device, applied on the fly) and
+//    three fused passes (k_proj: mdot, update + second dots, final + norm) followed
+//    by a one-thread Hessenberg/Givens kernel (k_arnoldi_step).
+//  * Reductions are deterministic: per-block partials in a fixed element
+//    assignment, summed in block order by the last block to finish (threadfence +
+//    counter).  Steps are queued without host round trips (a device `done` flag
+//    turns kernels queued past convergence into no-ops; the host looks every
+//    kHostCheck steps).
 #include <cuda_runtime.h>
 
 #include <algorithm>

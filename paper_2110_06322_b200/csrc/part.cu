@@ -131,20 +131,34 @@ __global__ void k_include(int nT, const TileHdr* tiles, const int* has, int* inc
   inc[t] = v;
 }
 
-// need[a] = 1 for every non-owned source of an included tile's fill runs
+// need[a] = 1 for every non-owned source of an included tile's fill runs;
+// bnd[t] = 1 for an included tile with such a source (a BOUNDARY tile: its extend
+// waits for the halo exchange), intr[t] = 1 for the other included tiles
 __global__ void k_need(const TileHdr* tiles, const int* inc, const uint64_t* runs, int64_t lo,
-                       int64_t hi, int* need) {
+                       int64_t hi, int* need, int* bnd, int* intr) {
   const int t = blockIdx.x;
-  if (!inc[t]) return;
-  const TileHdr T = tiles[t];
-  for (int r = T.r0 + threadIdx.x; r < T.r1; r += blockDim.x) {
-    const uint64_t run = runs[r];
-    const int64_t src = (uint32_t)run;
-    const int len = (int)((run >> 48) & 0xff);
-    for (int q = 0; q < len; ++q) {
-      const int64_t a = src + q;
-      if (a < lo || a >= hi) need[a] = 1;
+  __shared__ int any;
+  if (threadIdx.x == 0) any = 0;
+  __syncthreads();
+  if (inc[t]) {
+    const TileHdr T = tiles[t];
+    for (int r = T.r0 + threadIdx.x; r < T.r1; r += blockDim.x) {
+      const uint64_t run = runs[r];
+      const int64_t src = (uint32_t)run;
+      const int len = (int)((run >> 48) & 0xff);
+      for (int q = 0; q < len; ++q) {
+        const int64_t a = src + q;
+        if (a < lo || a >= hi) {
+          need[a] = 1;
+          any = 1;
+        }
+      }
     }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    bnd[t] = inc[t] && any;
+    intr[t] = inc[t] && !any;
   }
 }
 
@@ -191,16 +205,19 @@ __global__ void k_part_runs(int nT, const TileHdr* tiles, const int* inc, const 
   }
 }
 
-__global__ void k_part_tiles(int nT, const TileHdr* tiles, const int* inc, const int* incpos,
-                             int64_t lo, int64_t hi, const int64_t* runstart, TileHdr* sub,
-                             int* tmap) {
+// sub-band tile order: the interior tiles first (Morton order), then the boundary
+// tiles (Morton order), so the overlapped apply extends [0, nTint) while the halo
+// exchange is in flight
+__global__ void k_part_tiles(int nT, const TileHdr* tiles, const int* inc, const int* bnd,
+                             const int* intpos, const int* bndpos, int nInt, int64_t lo, int64_t hi,
+                             const int64_t* runstart, TileHdr* sub, int* tmap) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= nT) return;
   if (!inc[t]) {
     tmap[t] = -1;
     return;
   }
-  const int q = incpos[t];
+  const int q = bnd[t] ? nInt + bndpos[t] : intpos[t];
   tmap[t] = q;
   TileHdr T = tiles[t];
   const int64_t a0 = std::max<int64_t>(T.a0, lo), a1 = std::min<int64_t>(T.a1, hi);
@@ -279,10 +296,16 @@ int part_create(const cpm_band* B, int rank, int R, cudaStream_t s, cpm_part** o
   P->nOwned = P->hi - P->lo;
   for (int q = 0; q <= R; ++q) P->bounds.push_back((int64_t)q * nA / R);
 
-  DB has, inc, incpos, need, hpos, tmap;
+  DB has, inc, incpos, need, hpos, tmap, bnd, intr, bndpos, intpos;
   CPM_TRY(has.alloc(sizeof(int) * (nT + 1)));
   CPM_TRY(inc.alloc(sizeof(int) * (nT + 1)));
   CPM_TRY(incpos.alloc(sizeof(int) * (nT + 1)));
+  CPM_TRY(bnd.alloc(sizeof(int) * (nT + 1)));
+  CPM_TRY(intr.alloc(sizeof(int) * (nT + 1)));
+  CPM_TRY(bndpos.alloc(sizeof(int) * (nT + 1)));
+  CPM_TRY(intpos.alloc(sizeof(int) * (nT + 1)));
+  CPM_CUDA(cudaMemsetAsync(bnd.p, 0, sizeof(int) * (nT + 1), s));
+  CPM_CUDA(cudaMemsetAsync(intr.p, 0, sizeof(int) * (nT + 1), s));
   CPM_TRY(need.alloc(sizeof(int) * (nA + 1)));
   CPM_TRY(hpos.alloc(sizeof(int) * (nA + 1)));
   CPM_TRY(tmap.alloc(sizeof(int) * nT));
@@ -292,8 +315,13 @@ int part_create(const cpm_band* B, int rank, int R, cudaStream_t s, cpm_part** o
   k_include<<<(nT + 256) / 256, 256, 0, s>>>(nT, B->tiles, has.as<int>(), inc.as<int>());
   count_launch();
   CPM_TRY(scan(inc.as<int>(), incpos.as<int>(), nT + 1, s));
-  k_need<<<nT, 128, 0, s>>>(B->tiles, inc.as<int>(), B->runs, P->lo, P->hi, need.as<int>());
+  k_need<<<nT, 128, 0, s>>>(B->tiles, inc.as<int>(), B->runs, P->lo, P->hi, need.as<int>(), bnd.as<int>(),
+                            intr.as<int>());
   count_launch();
+  CPM_TRY(scan(bnd.as<int>(), bndpos.as<int>(), nT + 1, s));
+  CPM_TRY(scan(intr.as<int>(), intpos.as<int>(), nT + 1, s));
+  int nInt = 0;
+  CPM_TRY(read1(intpos.as<int>() + nT, &nInt, s));
   CPM_TRY(scan(need.as<int>(), hpos.as<int>(), nA + 1, s));
   int nTs = 0, nH = 0;
   CPM_TRY(read1(incpos.as<int>() + nT, &nTs, s));
@@ -324,6 +352,7 @@ int part_create(const cpm_band* B, int rank, int R, cudaStream_t s, cpm_part** o
   L.nA = P->nOwned;
   L.nE = B->nE;
   L.nT = nTs;
+  L.nTint = nInt;
   L.nRuns = nR;
   L.maxBox = B->maxBox;
   L.zeroFill = false;
@@ -341,8 +370,9 @@ int part_create(const cpm_band* B, int rank, int R, cudaStream_t s, cpm_part** o
                                        hpos.as<int>(), rstart.as<int64_t>(), nullptr, L.runs);
   count_launch();
   CPM_CUDA(cudaMalloc(&L.tiles, sizeof(TileHdr) * std::max(nTs, 1)));
-  k_part_tiles<<<(nT + 255) / 256, 256, 0, s>>>(nT, B->tiles, inc.as<int>(), incpos.as<int>(), P->lo,
-                                                P->hi, rstart.as<int64_t>(), L.tiles, tmap.as<int>());
+  k_part_tiles<<<(nT + 255) / 256, 256, 0, s>>>(nT, B->tiles, inc.as<int>(), bnd.as<int>(), intpos.as<int>(),
+                                                bndpos.as<int>(), nInt, P->lo, P->hi, rstart.as<int64_t>(),
+                                                L.tiles, tmap.as<int>());
   count_launch();
   k_remap_nbrs<<<(nTs + 255) / 256, 256, 0, s>>>(nTs, L.tiles, tmap.as<int>());
   count_launch();
@@ -443,6 +473,39 @@ int part_exchange(const cpm_part* P, const cpm_comm* comm, const double* x, cuda
                        P->sendOff, P->hbuf, P->recvCount, P->recvOff, s);
 }
 
+// y = A x on the owned slice.  With several ranks the halo exchange (gather + NCCL
+// send/recv, or the host transport) runs on a side stream while the interior tiles
+// (no halo source: [0, nTint) of the sub-band) are extended on s; the boundary tiles'
+// extend waits for the exchange, then the laplace of all tiles.  CPM_HALO_OVERLAP=0:
+// exchange, then the whole apply (A/B).
+int part_apply(const cpm_part* P, const cpm_comm* comm, double c, const double* x, double* y,
+               const double* scale, const int* skip, cudaStream_t s) {
+  static const bool overlap = [] {
+    const char* v = getenv("CPM_HALO_OVERLAP");
+    return !v || *v != '0';
+  }();
+  const cpm_band* L = &P->lb;
+  if (P->nranks == 1 || !overlap) {
+    CPM_TRY(part_exchange(P, comm, x, s));  // collective: always performed
+    return apply_device_split(L, c, x, P->hbuf, y, scale, 0, s, skip);
+  }
+  cpm_part* mp = const_cast<cpm_part*>(P);
+  if (!mp->xs) {
+    CPM_CUDA(cudaStreamCreateWithFlags(&mp->xs, cudaStreamNonBlocking));
+    CPM_CUDA(cudaEventCreateWithFlags(&mp->xev[0], cudaEventDisableTiming));
+    CPM_CUDA(cudaEventCreateWithFlags(&mp->xev[1], cudaEventDisableTiming));
+  }
+  CPM_CUDA(cudaEventRecord(mp->xev[0], s));  // x produced; the previous apply read hbuf
+  CPM_CUDA(cudaStreamWaitEvent(mp->xs, mp->xev[0], 0));
+  if (L->nT > 0) CPM_TRY(extend_tiles(L, x, P->hbuf, s, skip, 0, L->nTint));
+  CPM_TRY(part_exchange(P, comm, x, mp->xs));
+  CPM_CUDA(cudaEventRecord(mp->xev[1], mp->xs));
+  CPM_CUDA(cudaStreamWaitEvent(s, mp->xev[1], 0));
+  if (L->nT == 0) return CPM_OK;
+  CPM_TRY(extend_tiles(L, x, P->hbuf, s, skip, L->nTint, L->nT));
+  return laplace_tiles(L, c, x, y, scale, 0, s, skip);
+}
+
 }  // namespace cpm
 
 cpm_comm::~cpm_comm() {
@@ -453,6 +516,9 @@ cpm_part::~cpm_part() {
   void* ps[] = {lb.tiles, lb.runs, lb.vb, lb.acell, halo, hbuf, sendidx, sendbuf, rdstage};
   for (void* p : ps)
     if (p) cudaFree(p);
+  if (xs) cudaStreamDestroy(xs);
+  for (cudaEvent_t e : xev)
+    if (e) cudaEventDestroy(e);
   lb.tiles = nullptr;
   delete ws;
 }
@@ -520,6 +586,7 @@ int cpm_part_get_info(const cpm_part* p, cpm_part_info* info) {
   info->n_halo = p->nHalo;
   info->n_tiles = p->lb.nT;
   info->n_send = p->nSend;
+  info->n_interior_tiles = p->lb.nTint;
   return CPM_OK;
 }
 
@@ -548,9 +615,8 @@ int cpm_part_apply(const cpm_part* p, const cpm_comm* comm, double c, const doub
   if (!p || !u_owned || !y_owned) return fail(CPM_ERR_ARG, "cpm_part_apply: null argument");
   if (!is_device_ptr(u_owned) || !is_device_ptr(y_owned))
     return fail(CPM_ERR_ARG, "cpm_part_apply: vectors must be device memory");
-  cudaStream_t s = (cudaStream_t)stream;
-  CPM_TRY(part_exchange(p, comm, u_owned, s));
-  return apply_device_split(&p->lb, c, u_owned, p->hbuf, y_owned, nullptr, 0, s);
+  if (p->nranks > 1 && !comm) return fail(CPM_ERR_ARG, "cpm_part_apply: needs a communicator");
+  return part_apply(p, comm, c, u_owned, y_owned, nullptr, nullptr, (cudaStream_t)stream);
 }
 
 static int part_solve(const cpm_part* p, const cpm_comm* comm, double c, const double* f_owned,
@@ -608,8 +674,7 @@ static int part_solve(const cpm_part* p, const cpm_comm* comm, double c, const d
   LinOp A;
   A.apply = [p, comm, c](const double* x, double* y, const double* scale, const int* skip,
                          cudaStream_t st) {
-    CPM_TRY(part_exchange(p, comm, x, st));  // collective: always performed
-    return apply_device_split(&p->lb, c, x, p->hbuf, y, scale, 0, st, skip);
+    return part_apply(p, comm, c, x, y, scale, skip, st);  // the exchange is collective: always performed
   };
   A.allreduce = [comm](double* buf, size_t n, cudaStream_t st) { return comm_allreduce_sum(comm, buf, n, st); };
   cpm_solve_stats local;

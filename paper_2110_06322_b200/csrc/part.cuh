@@ -28,6 +28,8 @@ struct cpm_part {
   std::vector<int64_t> sendCount, sendOff, recvCount, recvOff;
   cpm::Workspace* ws = nullptr;
   double* rdstage = nullptr;                   // 2 * nOwned: right-hand sides of cpm_part_rd_step
+  cudaStream_t xs = nullptr;                   // side stream of the overlapped halo exchange
+  cudaEvent_t xev[2] = {nullptr, nullptr};
   ~cpm_part();
 };
 
@@ -36,6 +38,10 @@ int rd_rhs_device(int64_t n, const double* u, const double* v, const cpm_rd_para
                   double c2, double* ru, double* rv, cudaStream_t s);
 int comm_allreduce_sum(const cpm_comm* comm, double* buf, size_t n, cudaStream_t s);
 int part_exchange(const cpm_part* P, const cpm_comm* comm, const double* x, cudaStream_t s);
+// exchange + apply of the partitioned operator, the halo exchange overlapped with the
+// extend of the interior tiles (part.cu)
+int part_apply(const cpm_part* P, const cpm_comm* comm, double c, const double* x, double* y,
+               const double* scale, const int* skip, cudaStream_t s);
 int halo_exchange(const cpm_comm* comm, int rank, int nranks, const double* x, int64_t nSend,
                   const int64_t* sendidx, double* sendbuf, const std::vector<int64_t>& sendCount,
                   const std::vector<int64_t>& sendOff, double* recvbuf,

@@ -581,8 +581,8 @@ static __global__ void __launch_bounds__(256) k_dcgs_dots_bulk(Seg S, int k, con
 // tile's u_j and z (L1 hits after the first warp).  Fixed association order: per
 // lane the tiles in order, then the warp shuffle tree, then the blocks in index
 // order (the last block of the segment, as k_dcgs_dots).  KW = max columns per warp.
-template <int KW, class Epi = NoEpi>
-static __global__ void __launch_bounds__(256, 2) k_dcgs_dots_direct(
+template <int KW, int MINB, int UN, class Epi = NoEpi>
+static __global__ void __launch_bounds__(256, MINB) k_dcgs_dots_direct(
     Seg S, int k, const double* __restrict__ V, int64_t ldv, const double* __restrict__ z, double* partial,
     int pld, double* out, int ldo, unsigned* counters, const int* __restrict__ skip, Epi epi = Epi()) {
   constexpr int TB = 256, NW = TB / 32, TE = 128;
@@ -599,38 +599,77 @@ static __global__ void __launch_bounds__(256, 2) k_dcgs_dots_direct(
   for (int c = 0; c < KW; ++c) a1[c] = a2[c] = 0.0;
   const bool vec2 = ((o0 | ldv) & 1) == 0;  // 16-byte aligned columns
   const int64_t stride = (int64_t)S.gps * TE;
-  for (int64_t t0 = (int64_t)lb * TE; t0 < n; t0 += stride) {
-    const int64_t e0 = t0 + 2 * lane, e1 = t0 + 64 + 2 * lane;
-    double u0, u1, u2, u3, z0, z1, z2, z3;
-    const bool full = t0 + TE <= n;
-    if (full && vec2) {
-      const double2 ua = __ldg((const double2*)(uj + e0)), ub = __ldg((const double2*)(uj + e1));
-      const double2 za = __ldg((const double2*)(zz + e0)), zb = __ldg((const double2*)(zz + e1));
-      u0 = ua.x; u1 = ua.y; u2 = ub.x; u3 = ub.y;
-      z0 = za.x; z1 = za.y; z2 = zb.x; z3 = zb.y;
-    } else {
-      u0 = e0 < n ? __ldg(uj + e0) : 0.0; u1 = e0 + 1 < n ? __ldg(uj + e0 + 1) : 0.0;
-      u2 = e1 < n ? __ldg(uj + e1) : 0.0; u3 = e1 + 1 < n ? __ldg(uj + e1 + 1) : 0.0;
-      z0 = e0 < n ? __ldg(zz + e0) : 0.0; z1 = e0 + 1 < n ? __ldg(zz + e0 + 1) : 0.0;
-      z2 = e1 < n ? __ldg(zz + e1) : 0.0; z3 = e1 + 1 < n ? __ldg(zz + e1 + 1) : 0.0;
+  // UN tiles per iteration (all their loads issued before the FMAs); per lane the
+  // tiles are still summed in increasing order
+  for (int64_t tb = (int64_t)lb * TE; tb < n; tb += (UN > 0 ? UN : 1) * stride) {
+    constexpr int UQ = UN > 0 ? UN : 1;
+    double u[UQ][4], zv[UQ][4];
+#pragma unroll
+    for (int q = 0; q < UQ; ++q) {
+      const int64_t t0 = tb + q * stride;
+      const int64_t e0 = t0 + 2 * lane, e1 = t0 + 64 + 2 * lane;
+      if (t0 + TE <= n && vec2) {
+        const double2 ua = __ldg((const double2*)(uj + e0)), ub = __ldg((const double2*)(uj + e1));
+        const double2 za = __ldg((const double2*)(zz + e0)), zb = __ldg((const double2*)(zz + e1));
+        u[q][0] = ua.x; u[q][1] = ua.y; u[q][2] = ub.x; u[q][3] = ub.y;
+        zv[q][0] = za.x; zv[q][1] = za.y; zv[q][2] = zb.x; zv[q][3] = zb.y;
+      } else {
+        u[q][0] = e0 < n ? __ldg(uj + e0) : 0.0; u[q][1] = e0 + 1 < n ? __ldg(uj + e0 + 1) : 0.0;
+        u[q][2] = e1 < n ? __ldg(uj + e1) : 0.0; u[q][3] = e1 + 1 < n ? __ldg(uj + e1 + 1) : 0.0;
+        zv[q][0] = e0 < n ? __ldg(zz + e0) : 0.0; zv[q][1] = e0 + 1 < n ? __ldg(zz + e0 + 1) : 0.0;
+        zv[q][2] = e1 < n ? __ldg(zz + e1) : 0.0; zv[q][3] = e1 + 1 < n ? __ldg(zz + e1 + 1) : 0.0;
+      }
+    }
+    if (UN == 0) {  // one tile, every owned column's loads issued before the FMAs
+      const int64_t e0 = tb + 2 * lane, e1 = tb + 64 + 2 * lane;
+      const bool fv = tb + TE <= n && vec2;
+      double v[KW][4];
+#pragma unroll
+      for (int c = 0; c < KW; ++c) {
+        const int i = warp + c * NW;
+        const double* col = V + (size_t)min(i, k - 1) * ldv + o0;
+        if (fv) {
+          const double2 va = __ldcs((const double2*)(col + e0)), vb = __ldcs((const double2*)(col + e1));
+          v[c][0] = va.x; v[c][1] = va.y; v[c][2] = vb.x; v[c][3] = vb.y;
+        } else {
+          v[c][0] = e0 < n ? __ldcs(col + e0) : 0.0; v[c][1] = e0 + 1 < n ? __ldcs(col + e0 + 1) : 0.0;
+          v[c][2] = e1 < n ? __ldcs(col + e1) : 0.0; v[c][3] = e1 + 1 < n ? __ldcs(col + e1 + 1) : 0.0;
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < KW; ++c)
+#pragma unroll
+        for (int x = 0; x < 4; ++x) {
+          a1[c] = fma(v[c][x], u[0][x], a1[c]);
+          a2[c] = fma(v[c][x], zv[0][x], a2[c]);
+        }
+      continue;
     }
 #pragma unroll
     for (int c = 0; c < KW; ++c) {
       const int i = warp + c * NW;
       if (i < k) {
         const double* col = V + (size_t)i * ldv + o0;
-        double v0, v1, v2, v3;
-        if (full && vec2) {
-          const double2 va = __ldcs((const double2*)(col + e0)), vb = __ldcs((const double2*)(col + e1));
-          v0 = va.x; v1 = va.y; v2 = vb.x; v3 = vb.y;
-        } else {
-          v0 = e0 < n ? __ldcs(col + e0) : 0.0; v1 = e0 + 1 < n ? __ldcs(col + e0 + 1) : 0.0;
-          v2 = e1 < n ? __ldcs(col + e1) : 0.0; v3 = e1 + 1 < n ? __ldcs(col + e1 + 1) : 0.0;
+        double v[UQ][4];
+#pragma unroll
+        for (int q = 0; q < UQ; ++q) {
+          const int64_t t0 = tb + q * stride;
+          const int64_t e0 = t0 + 2 * lane, e1 = t0 + 64 + 2 * lane;
+          if (t0 + TE <= n && vec2) {
+            const double2 va = __ldcs((const double2*)(col + e0)), vb = __ldcs((const double2*)(col + e1));
+            v[q][0] = va.x; v[q][1] = va.y; v[q][2] = vb.x; v[q][3] = vb.y;
+          } else {
+            v[q][0] = e0 < n ? __ldcs(col + e0) : 0.0; v[q][1] = e0 + 1 < n ? __ldcs(col + e0 + 1) : 0.0;
+            v[q][2] = e1 < n ? __ldcs(col + e1) : 0.0; v[q][3] = e1 + 1 < n ? __ldcs(col + e1 + 1) : 0.0;
+          }
         }
-        a1[c] = fma(v0, u0, a1[c]); a2[c] = fma(v0, z0, a2[c]);
-        a1[c] = fma(v1, u1, a1[c]); a2[c] = fma(v1, z1, a2[c]);
-        a1[c] = fma(v2, u2, a1[c]); a2[c] = fma(v2, z2, a2[c]);
-        a1[c] = fma(v3, u3, a1[c]); a2[c] = fma(v3, z3, a2[c]);
+#pragma unroll
+        for (int q = 0; q < UQ; ++q)
+#pragma unroll
+          for (int x = 0; x < 4; ++x) {
+            a1[c] = fma(v[q][x], u[q][x], a1[c]);
+            a2[c] = fma(v[q][x], zv[q][x], a2[c]);
+          }
       }
     }
   }
@@ -951,12 +990,28 @@ inline int launch_dcgs_dots_epi(const vec::Seg& S, int k, const double* V, int64
     const char* v = getenv("CPM_DOTS_DIRECT");
     return !v || *v != '0';
   }();
-  if (direct && k <= 8 * 8) {
-    CPM_CUDA(launch_pdl(vec::k_dcgs_dots_direct<8, Epi>, dim3(grid), dim3(256), 0, st, S, k, V, ldv, z, partial,
-                        pld, out, ldo, counters, skip, epi));
+  static const int dvar = [] {  // CPM_DOTS_VAR: 0 = 2 blocks/SM x 2 tiles, 1 = 2 x 1, 2 = 3 x 1 (A/B)
+    const char* v = getenv("CPM_DOTS_VAR");
+    return v ? atoi(v) : 0;
+  }();
+  if (direct && k <= 8 * 8 && dvar == 0) {
+    CPM_CUDA(launch_pdl(vec::k_dcgs_dots_direct<8, 2, 2, Epi>, dim3(grid), dim3(256), 0, st, S, k, V, ldv, z,
+                        partial, pld, out, ldo, counters, skip, epi));
+  } else if (direct && k <= 8 * 8 && dvar == 1) {
+    CPM_CUDA(launch_pdl(vec::k_dcgs_dots_direct<8, 2, 1, Epi>, dim3(grid), dim3(256), 0, st, S, k, V, ldv, z,
+                        partial, pld, out, ldo, counters, skip, epi));
+  } else if (direct && k <= 8 * 8 && dvar == 2) {
+    CPM_CUDA(launch_pdl(vec::k_dcgs_dots_direct<8, 2, 0, Epi>, dim3(grid), dim3(256), 0, st, S, k, V, ldv, z,
+                        partial, pld, out, ldo, counters, skip, epi));
+  } else if (direct && k <= 8 * 4 && dvar == 3) {
+    CPM_CUDA(launch_pdl(vec::k_dcgs_dots_direct<4, 2, 0, Epi>, dim3(grid), dim3(256), 0, st, S, k, V, ldv, z,
+                        partial, pld, out, ldo, counters, skip, epi));
+  } else if (direct && k <= 8 * 8 && dvar == 3) {
+    CPM_CUDA(launch_pdl(vec::k_dcgs_dots_direct<8, 2, 0, Epi>, dim3(grid), dim3(256), 0, st, S, k, V, ldv, z,
+                        partial, pld, out, ldo, counters, skip, epi));
   } else if (direct && k <= 8 * 17) {
-    CPM_CUDA(launch_pdl(vec::k_dcgs_dots_direct<17, Epi>, dim3(grid), dim3(256), 0, st, S, k, V, ldv, z, partial,
-                        pld, out, ldo, counters, skip, epi));
+    CPM_CUDA(launch_pdl(vec::k_dcgs_dots_direct<17, 2, 1, Epi>, dim3(grid), dim3(256), 0, st, S, k, V, ldv, z,
+                        partial, pld, out, ldo, counters, skip, epi));
   } else if (bulk && k <= 52) {  // a stage of (k+1) 2 KB columns: two blocks per SM
     const size_t stage = (size_t)(k + 1) * (256 + 4) * sizeof(double);
     const int ns = depth(stage);

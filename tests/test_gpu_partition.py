@@ -53,6 +53,11 @@ def test_partitioned_apply_bit_exact(cpm, kind, h, R):
         y_cat[p.lo:p.hi] = y_own
     torch.cuda.synchronize()
     assert torch.equal(y_cat, y)
+    # sub-band tiles: [0, n_interior_tiles) read no halo node (extended while the halo
+    # exchange is in flight), every rank of R >= 2 has boundary tiles
+    for p in parts:
+        assert 0 <= p.n_interior_tiles < p.n_tiles
+
     # send plan = inverse of the receive plans (what exchange_requests computes)
     for r, p in enumerate(parts):
         send = [halos[q][owners(halos[q], bounds) == r] for q in range(R)]
