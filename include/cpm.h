@@ -114,7 +114,8 @@ int cpm_band_active_coords(const cpm_band* band, int32_t* ijk_host);
 int cpm_band_ghost_coords(const cpm_band* band, int32_t* ijk_host);
 /* Diagnostics of the extend's node order (build.cu k_warp_order; DESIGN.md
  * §Kernels): per tile 6 int32 into tiles_host[6*n_tiles] = e0, e1 (eval-node
- * range, padded index space), np (equal-base pairs at e0 + 2p, e0 + 2p + 1),
+ * range, padded index space), np | nd << 16 (np equal-base pairs at e0 + 2p,
+ * e0 + 2p + 1; then nd unpaired nodes gathered by lane pairs, the rest one per lane),
  * row stride and plane stride of the tile's stencil box, box cells; and, if
  * eoff_host is not null, the packed stencil-base offsets (low 16 bits: offset
  * in the box, high 16: brick cell) of the padded eval index space [0, e1 of the

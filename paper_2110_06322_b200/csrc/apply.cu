@@ -104,17 +104,20 @@ __device__ __forceinline__ void st_hint(double* p, double v, uint64_t pol) {
   asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;\n" ::"l"(p), "d"(v), "l"(pol) : "memory");
 }
 
-// Slot s of a tile (thread tid handles slots tid + 128 k): nodes 0 .. 2np-1 (equal-
-// base pairs, build.cu k_warp_order) one per slot; the unpaired nodes two slots
-// each (both lanes of a lane pair gather the same stencil, the even one writes),
-// so every adjacent lane pair of a warp reads one address: one-wavefront gathers.
-__device__ __forceinline__ int slot_node(int s, int np2, bool& write) {
-  if (s < np2) {
-    write = true;
-    return s;
+// Slot s of a tile (thread tid handles slots tid + 128 k; build.cu k_warp_order):
+// nodes 0 .. 2np-1 (equal-base pairs) one per slot, every adjacent lane pair reading
+// one address (16 distinct doubles per warp: one wavefront); the nd unpaired nodes
+// that complete the last pair warp two slots each (both lanes gather, the even one
+// writes); the other unpaired nodes one per slot (32 distinct doubles, two
+// wavefronts, but half the instructions of a duplicated node).
+__device__ __forceinline__ int slot_node(int s, int np2, int nd, bool& write) {
+  write = true;
+  if (s < np2) return s;
+  if (s < np2 + 2 * nd) {
+    write = ((s - np2) & 1) == 0;
+    return np2 + ((s - np2) >> 1);
   }
-  write = ((s - np2) & 1) == 0;
-  return np2 + ((s - np2) >> 1);
+  return s - nd;
 }
 
 __device__ __forceinline__ void contract_node(const double (&tn)[3], uint32_t eo,
@@ -156,7 +159,7 @@ __global__ void __launch_bounds__(kNtThreads, 8)
   const int t = tbase + (int)blockIdx.x, tid = threadIdx.x;  // tiles [tbase, tend)
   const TileHdr* T = tiles + t;
   const int e0 = T->e0, ne = T->e1 - e0, r0 = T->r0, r1 = T->r1;
-  const int np2 = 2 * T->np, nslot = 2 * ne - np2;
+  const int np2 = 2 * T->np, nd = T->pad2, nslot = ne + nd;
   const int sx = T->pad[0], sxy = T->pad[1];
   const uint64_t pfirst = policy_evict_first(), plast = policy_evict_last();
   // the first kNtPre slots of this thread are requested before the box is staged
@@ -167,7 +170,7 @@ __global__ void __launch_bounds__(kNtThreads, 8)
     const int sl = tid + k * kNtThreads;
     if (sl < nslot) {
       bool w;
-      const int i = e0 + slot_node(sl, np2, w);
+      const int i = e0 + slot_node(sl, np2, nd, w);
       nt[k][0] = ld_hint(tx + i, pfirst);
       nt[k][1] = ld_hint(ty + i, pfirst);
       nt[k][2] = ld_hint(tz + i, pfirst);
@@ -228,13 +231,13 @@ __global__ void __launch_bounds__(kNtThreads, 8)
     const int sl = tid + k * kNtThreads;
     if (sl < nslot) {
       bool w;
-      slot_node(sl, np2, w);
+      slot_node(sl, np2, nd, w);
       contract_node(nt[k], eo[k], box, sx, sxy, out, w, plast);
     }
   }
   for (int sl = tid + kNtPre * kNtThreads; sl < nslot; sl += kNtThreads) {
     bool w;
-    const int i = e0 + slot_node(sl, np2, w);
+    const int i = e0 + slot_node(sl, np2, nd, w);
     double tn[3] = {ld_hint(tx + i, pfirst), ld_hint(ty + i, pfirst), ld_hint(tz + i, pfirst)};
     contract_node(tn, ld_hint(eoff + i, pfirst), box, sx, sxy, out, w, plast);
   }

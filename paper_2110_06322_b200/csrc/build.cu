@@ -369,7 +369,7 @@ __global__ void __launch_bounds__(512) k_warp_order(TileHdr* tiles, double* tx, 
   __shared__ uint32_t so[512];
   __shared__ uint16_t perm[512], pfirst[256], single[512];
   __shared__ uint8_t pused[512];
-  __shared__ int npair;
+  __shared__ int npair, ndup;
   __shared__ unsigned long long best;
   const TileHdr T = tiles[blockIdx.x];
   const int n = T.e1 - T.e0, t = threadIdx.x;
@@ -441,20 +441,19 @@ __global__ void __launch_bounds__(512) k_warp_order(TileHdr* tiles, double* tx, 
       i = j;
     }
     npair = np;
-    // warps of 16 items (a pair, or an unpaired node on both lanes of a lane pair):
-    // pairs first, the warp in progress continues with the unpaired nodes
-    int out = 0, taken = 0;
+    // warps of 16 items (a pair on a lane pair; the unpaired nodes that complete the
+    // last pair warp on both lanes of a lane pair): pairs first
+    int out = 0, taken = 0, nd = 0;
     uint32_t res = 0;
     uint16_t toff[16];
-    for (int phase = 0; phase < 2; ++phase) {
-      const int m = phase == 0 ? np : ns;
-      for (int q = 0; q < m; ++q) pused[q] = 0;
-      int first = 0, left = m;
+    for (int q = 0; q < np; ++q) pused[q] = 0;
+    {
+      int first = 0, left = np;
       while (left > 0) {
         for (int pass = 0; pass < 2 && taken < 16; ++pass) {  // compatible first, then any
-          for (int q = first; q < m && taken < 16; ++q) {
+          for (int q = first; q < np && taken < 16; ++q) {
             if (pused[q]) continue;
-            const int node = phase == 0 ? pfirst[q] : single[q];
+            const int node = pfirst[q];
             const uint32_t o = so[node] & 0xffffu, r = o & 15u;
             if (pass == 0) {
               bool ok = !((res >> r) & 1u);
@@ -466,16 +465,57 @@ __global__ void __launch_bounds__(512) k_warp_order(TileHdr* tiles, double* tx, 
             pused[q] = 1;
             --left;
             perm[out++] = (uint16_t)node;
-            if (phase == 0) perm[out++] = (uint16_t)(node + 1);
+            perm[out++] = (uint16_t)(node + 1);
           }
         }
-        while (first < m && pused[first]) ++first;
+        while (first < np && pused[first]) ++first;
         if (taken == 16) {
           taken = 0;
           res = 0;
         }
       }
     }
+    for (int q = 0; q < ns; ++q) pused[q] = 0;
+    int sleft = ns;
+    // the partial last pair warp: completed with unpaired nodes on lane pairs (dup)
+    while (taken > 0 && taken < 16 && sleft > 0) {
+      int pick = -1;
+      for (int q = 0; q < ns && pick < 0; ++q)
+        if (!pused[q] && !((res >> (so[single[q]] & 15u)) & 1u)) pick = q;
+      for (int q = 0; q < ns && pick < 0; ++q)
+        if (!pused[q]) pick = q;
+      pused[pick] = 1;
+      --sleft;
+      res |= 1u << (so[single[pick]] & 15u);
+      ++taken;
+      ++nd;
+      perm[out++] = single[pick];
+    }
+    // the other unpaired nodes one per lane, 16 per half-warp with distinct residues
+    // (16 distinct doubles of a half-warp in distinct bank pairs: one wavefront)
+    taken = 0;
+    res = 0;
+    int first = 0;
+    while (sleft > 0) {
+      for (int pass = 0; pass < 2 && taken < 16 && sleft > 0; ++pass) {
+        for (int q = first; q < ns && taken < 16; ++q) {
+          if (pused[q]) continue;
+          const uint32_t r = so[single[q]] & 15u;
+          if (pass == 0 && ((res >> r) & 1u)) continue;
+          res |= 1u << r;
+          ++taken;
+          pused[q] = 1;
+          --sleft;
+          perm[out++] = single[q];
+        }
+      }
+      while (first < ns && pused[first]) ++first;
+      if (taken == 16) {
+        taken = 0;
+        res = 0;
+      }
+    }
+    ndup = nd;
   }
   __syncthreads();
   if (t < n) {
@@ -485,7 +525,10 @@ __global__ void __launch_bounds__(512) k_warp_order(TileHdr* tiles, double* tx, 
     tz[T.e0 + t] = sv[2][o];
     eoff[T.e0 + t] = so[o];
   }
-  if (t == 0) tiles[blockIdx.x].np = npair;
+  if (t == 0) {
+    tiles[blockIdx.x].np = npair;
+    tiles[blockIdx.x].pad2 = ndup;
+  }
 }
 
 // ------------------------------------------------------------------ B7

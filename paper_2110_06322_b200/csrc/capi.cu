@@ -180,7 +180,7 @@ int cpm_band_eval_order(const cpm_band* b, int32_t* tiles_host, uint32_t* eoff_h
     int32_t* o = tiles_host + 6 * t;
     o[0] = T[t].e0;
     o[1] = T[t].e1;
-    o[2] = T[t].np;
+    o[2] = T[t].np | (T[t].pad2 << 16);
     o[3] = T[t].pad[0];
     o[4] = T[t].pad[1];
     o[5] = T[t].pad[1] * T[t].sz;

@@ -85,7 +85,7 @@ struct TileHdr {
   int32_t pad[3];      // row stride, plane stride of the box; segment id (RAS)
   uint32_t emask[16];  // eval-node cells of the brick (Sigma_A u Sigma_G), bit = cell
   int32_t np;          // eval nodes e0 + 2p, e0 + 2p + 1 (p < np) share a stencil base
-  int32_t pad2;
+  int32_t pad2;        // nd: unpaired nodes 2np .. 2np+nd-1 run on lane pairs (the rest one per lane)
 };
 static_assert(sizeof(TileHdr) == 168, "TileHdr layout");
 

@@ -986,27 +986,25 @@ inline int launch_dcgs_dots_epi(const vec::Seg& S, int k, const double* V, int64
     const char* v = getenv("CPM_DOTS_BULK");
     return !v || *v != '0';
   }();
-  static const bool direct = [] {  // CPM_DOTS_DIRECT=0: the staged kernels (A/B)
+  static const bool direct_env = [] {  // CPM_DOTS_DIRECT=0: the staged kernels (A/B)
     const char* v = getenv("CPM_DOTS_DIRECT");
     return !v || *v != '0';
   }();
-  static const int dvar = [] {  // CPM_DOTS_VAR: 0 = 2 blocks/SM x 2 tiles, 1 = 2 x 1, 2 = 3 x 1 (A/B)
-    const char* v = getenv("CPM_DOTS_VAR");
-    return v ? atoi(v) : 0;
-  }();
-  if (direct && k <= 8 * 8 && dvar == 0) {
-    CPM_CUDA(launch_pdl(vec::k_dcgs_dots_direct<8, 2, 2, Epi>, dim3(grid), dim3(256), 0, st, S, k, V, ldv, z,
+  // the register-direct kernel for the single-segment (global) GMRES, whose columns are
+  // 16-byte aligned; the RAS segments start at arbitrary elements: the bulk-staged kernel
+  const bool direct = direct_env && S.nseg == 1;
+  // register-direct reduction pass: every owned column's loads of a tile issued
+  // before its FMAs (UN = 0), columns per warp KW by k (fewer registers for small k)
+  if (direct && k <= 8 * 2) {
+    CPM_CUDA(launch_pdl(vec::k_dcgs_dots_direct<2, 2, 0, Epi>, dim3(grid), dim3(256), 0, st, S, k, V, ldv, z,
                         partial, pld, out, ldo, counters, skip, epi));
-  } else if (direct && k <= 8 * 8 && dvar == 1) {
-    CPM_CUDA(launch_pdl(vec::k_dcgs_dots_direct<8, 2, 1, Epi>, dim3(grid), dim3(256), 0, st, S, k, V, ldv, z,
-                        partial, pld, out, ldo, counters, skip, epi));
-  } else if (direct && k <= 8 * 8 && dvar == 2) {
-    CPM_CUDA(launch_pdl(vec::k_dcgs_dots_direct<8, 2, 0, Epi>, dim3(grid), dim3(256), 0, st, S, k, V, ldv, z,
-                        partial, pld, out, ldo, counters, skip, epi));
-  } else if (direct && k <= 8 * 4 && dvar == 3) {
+  } else if (direct && k <= 8 * 4) {
     CPM_CUDA(launch_pdl(vec::k_dcgs_dots_direct<4, 2, 0, Epi>, dim3(grid), dim3(256), 0, st, S, k, V, ldv, z,
                         partial, pld, out, ldo, counters, skip, epi));
-  } else if (direct && k <= 8 * 8 && dvar == 3) {
+  } else if (direct && k <= 8 * 6) {
+    CPM_CUDA(launch_pdl(vec::k_dcgs_dots_direct<6, 2, 0, Epi>, dim3(grid), dim3(256), 0, st, S, k, V, ldv, z,
+                        partial, pld, out, ldo, counters, skip, epi));
+  } else if (direct && k <= 8 * 8) {
     CPM_CUDA(launch_pdl(vec::k_dcgs_dots_direct<8, 2, 0, Epi>, dim3(grid), dim3(256), 0, st, S, k, V, ldv, z,
                         partial, pld, out, ldo, counters, skip, epi));
   } else if (direct && k <= 8 * 17) {

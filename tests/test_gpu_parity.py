@@ -77,24 +77,29 @@ def test_band_bit_exact(cpm, kind, h, kw):
 @pytest.mark.parametrize("kind,h,kw", CASES)
 def test_eval_order_invariants(cpm, kind, h, kw):
     """The extend's node order (build.cu k_warp_order): every
-    eval node once per tile, pairs share a stencil base, each warp of the extend
-    (32 slots; unpaired nodes on 2 slots) reads at most 16 distinct bases, every
-    stencil stays inside its tile's box."""
+    eval node once per tile, pairs share a stencil base, each warp of the pair
+    region (32 slots, the nd unpaired nodes completing its last warp on 2 slots)
+    reads at most 16 distinct bases, every stencil stays inside its tile's box."""
     gb = _gpu_band(cpm, kind, h, **kw)
     tiles, eoff = cpm.cpm_band_eval_order(gb)
     assert int((tiles[:, 1] - tiles[:, 0]).sum()) == gb.info.n_active + gb.info.n_ghost
-    for e0, e1, npair, sx, sxy, cells in tiles.astype(np.int64):
+    for e0, e1, npnd, sx, sxy, cells in tiles.astype(np.int64):
+        npair, nd = npnd & 0xFFFF, npnd >> 16
         ne = e1 - e0
-        assert e0 % 4 == 0 and 0 <= 2 * npair <= ne
+        assert e0 % 4 == 0 and 0 <= 2 * npair + nd <= ne and 0 <= nd < 16
         eo = eoff[e0:e1].astype(np.int64)
         base, cell = eo & 0xFFFF, eo >> 16
         assert np.all(cell < 512) and len(np.unique(cell)) == ne
         assert np.all(base + 3 * sxy + 3 * sx + 3 < cells)
         assert np.array_equal(base[0:2 * npair:2], base[1:2 * npair:2])
-        s = np.arange(2 * ne - 2 * npair)
-        node = np.where(s < 2 * npair, s, 2 * npair + (s - 2 * npair) // 2)
-        for w0 in range(0, len(s), 32):
+        np2 = 2 * npair
+        s = np.arange(ne + nd)
+        node = np.where(s < np2, s, np.where(s < np2 + 2 * nd, np2 + (s - np2) // 2, s - nd))
+        assert np.array_equal(np.unique(node), np.arange(ne))
+        for w0 in range(0, np2 + 2 * nd, 32):           # pair-region warps
             assert len(np.unique(base[node[w0:w0 + 32]])) <= 16
+        # the unpaired region starts on a warp boundary (or the tile's last warp)
+        assert (np2 + 2 * nd) % 32 == 0 or np2 + nd == ne
 
 
 @pytest.mark.parametrize("kind,h,kw", CASES)
