@@ -133,6 +133,16 @@ void cpm_band_free(cpm_band* band);
  * `stream` for device pointers; synchronous for host pointers.
  * Errors: CPM_ERR_ARG (null pointers / aliasing), CPM_ERR_CUDA. */
 int cpm_apply(const cpm_band* band, double c, const double* u, double* y, void* stream);
+/* cpm_apply_async — cpm_apply for PINNED host buffers (cudaMallocHost /
+ * cudaHostRegister), pipelined: the call enqueues the copy of u to the device, the
+ * apply (on `stream`) and the copy of y back, and returns; y is complete after
+ * cpm_apply_sync(band) (or a device synchronise).  Consecutive calls overlap (the
+ * copy-in of the next call with the apply and copy-out of this one; two staging
+ * slots owned by the band): u and y of a call must stay untouched until then.
+ * Device or pageable pointers: exactly cpm_apply (synchronous for host memory).
+ * Errors: those of cpm_apply. */
+int cpm_apply_async(const cpm_band* band, double c, const double* u, double* y, void* stream);
+int cpm_apply_sync(const cpm_band* band);
 
 /* ---------------------------------------------------------------- Krylov solve
  * cpm_solve — solve (c - Delta_S^h) u = f (Eq. 2) by restarted GMRES(restart)

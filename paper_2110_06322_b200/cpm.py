@@ -92,6 +92,8 @@ _SIGS = {
     "cpm_band_eval_order": (ctypes.c_int, [_vp, _vp, _vp]),
     "cpm_band_free": (None, [_vp]),
     "cpm_apply": (ctypes.c_int, [_vp, ctypes.c_double, _vp, _vp, _vp]),
+    "cpm_apply_async": (ctypes.c_int, [_vp, ctypes.c_double, _vp, _vp, _vp]),
+    "cpm_apply_sync": (ctypes.c_int, [_vp]),
     "cpm_solve": (ctypes.c_int, [_vp, ctypes.c_double, _vp, _vp, ctypes.c_double, ctypes.c_int,
                                  ctypes.c_int, _vp, ctypes.POINTER(_SolveStats), _vp]),
     "cpm_ras_setup": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, ctypes.c_int,
@@ -283,6 +285,18 @@ def cpm_apply(band: Band, c: float, u, y, stream=None):
     py, sy = _ptr_stream(y, band.n, True)
     _check(load_library().cpm_apply(band.handle, float(c), pu, py, stream or su or sy), "cpm_apply")
     return y
+
+
+def cpm_apply_async(band: Band, c: float, u, y, stream=None):
+    """Pipelined apply on pinned host buffers (include/cpm.h); y complete after cpm_apply_sync."""
+    pu, su = _ptr_stream(u, band.n, False)
+    py, sy = _ptr_stream(y, band.n, True)
+    _check(load_library().cpm_apply_async(band.handle, float(c), pu, py, stream or su or sy), "cpm_apply_async")
+    return y
+
+
+def cpm_apply_sync(band: Band):
+    _check(load_library().cpm_apply_sync(band.handle), "cpm_apply_sync")
 
 
 @dataclass

@@ -708,6 +708,19 @@ void free_workspace(Workspace* w);
 void free_band(cpm_band* b) {
   if (!b) return;
   if (b->ws) free_workspace(b->ws);
+  if (b->as) {
+    cpm_band::AsyncStage* a = b->as;
+    if (a->out) cudaStreamSynchronize(a->out);
+    for (int q = 0; q < 2; ++q) {
+      if (a->u[q]) cudaFree(a->u[q]);
+      if (a->y[q]) cudaFree(a->y[q]);
+      for (cudaEvent_t e : {a->ein[q], a->ek[q], a->eout[q]})
+        if (e) cudaEventDestroy(e);
+    }
+    if (a->in) cudaStreamDestroy(a->in);
+    if (a->out) cudaStreamDestroy(a->out);
+    delete a;
+  }
   if (b->owns) {
     void* ptrs[] = {b->tiles, b->tx,      b->ty,      b->tz,    b->eoff, b->acell,
                     b->aijk,  b->gijk,    b->runs,    b->vb,    b->dstage0, b->dstage1,
@@ -960,6 +973,9 @@ int build_band(const cpm_surface* surf, double h, int p, double L, cudaStream_t 
   B->nRuns = totRuns;
 
   CPM_TRY(dalloc_owned(&B->vb, (size_t)totT * kBrickCells, &B->bytes, "vb"));
+  // cells outside Sigma_A u Sigma_G are never written by the extend; k_laplace loads
+  // whole slots (never using those cells): defined values for them
+  CPM_CUDA(cudaMemsetAsync(B->vb, 0, sizeof(double) * (size_t)totT * kBrickCells, s));
   CPM_CUDA(cudaStreamSynchronize(s));
   *out = guard.release();
   return CPM_OK;

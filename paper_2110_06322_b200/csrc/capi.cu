@@ -214,6 +214,66 @@ int cpm_apply(const cpm_band* b, double c, const double* u, double* y, void* str
   return CPM_OK;
 }
 
+static bool is_pinned_host(const void* p) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost;
+}
+
+// Pipelined host-buffer apply: call i copies u in on the copy-in stream, applies on
+// the caller's stream, copies y out on the copy-out stream, through staging slot
+// i % 2, and returns.  The copy-in of call i+1 waits only for the kernels of call
+// i-1 (its slot's previous reader), so it overlaps call i's apply and copy-out: the
+// two directions of the PCIe link and the kernels run concurrently.
+int cpm_apply_async(const cpm_band* b, double c, const double* u, double* y, void* stream) {
+  if (!b || !u || !y) return fail(CPM_ERR_ARG, "cpm_apply_async: null argument");
+  if ((const void*)u == (const void*)y) return fail(CPM_ERR_ARG, "cpm_apply_async: u and y must not alias");
+  if (!is_pinned_host(u) || !is_pinned_host(y)) return cpm_apply(b, c, u, y, stream);
+  cudaStream_t s = (cudaStream_t)stream;
+  cpm_band* mb = const_cast<cpm_band*>(b);
+  if (!mb->as) {
+    auto* a = new cpm_band::AsyncStage();
+    mb->as = a;
+    for (int q = 0; q < 2; ++q) {
+      CPM_CUDA(cudaMalloc(&a->u[q], sizeof(double) * std::max<int64_t>(b->nA, 1)));
+      CPM_CUDA(cudaMalloc(&a->y[q], sizeof(double) * std::max<int64_t>(b->nA, 1)));
+      CPM_CUDA(cudaEventCreateWithFlags(&a->ein[q], cudaEventDisableTiming));
+      CPM_CUDA(cudaEventCreateWithFlags(&a->ek[q], cudaEventDisableTiming));
+      CPM_CUDA(cudaEventCreateWithFlags(&a->eout[q], cudaEventDisableTiming));
+      CPM_CUDA(cudaEventRecord(a->ek[q], s));
+      CPM_CUDA(cudaEventRecord(a->eout[q], s));
+    }
+    CPM_CUDA(cudaStreamCreateWithFlags(&a->in, cudaStreamNonBlocking));
+    CPM_CUDA(cudaStreamCreateWithFlags(&a->out, cudaStreamNonBlocking));
+  }
+  cpm_band::AsyncStage* a = mb->as;
+  const int q = (int)(a->calls++ & 1u);
+  const size_t bytes = sizeof(double) * b->nA;
+  CPM_CUDA(cudaStreamWaitEvent(a->in, a->ek[q], 0));      // slot q's previous apply has read u
+  CPM_CUDA(cudaMemcpyAsync(a->u[q], u, bytes, cudaMemcpyHostToDevice, a->in));
+  CPM_CUDA(cudaEventRecord(a->ein[q], a->in));
+  CPM_CUDA(cudaStreamWaitEvent(s, a->ein[q], 0));
+  CPM_CUDA(cudaStreamWaitEvent(s, a->eout[q], 0));        // slot q's previous y has been copied out
+  CPM_TRY(apply_device(b, c, a->u[q], a->y[q], nullptr, 0, s));
+  CPM_CUDA(cudaEventRecord(a->ek[q], s));
+  CPM_CUDA(cudaStreamWaitEvent(a->out, a->ek[q], 0));
+  CPM_CUDA(cudaMemcpyAsync(y, a->y[q], bytes, cudaMemcpyDeviceToHost, a->out));
+  CPM_CUDA(cudaEventRecord(a->eout[q], a->out));
+  return CPM_OK;
+}
+
+int cpm_apply_sync(const cpm_band* b) {
+  if (!b) return fail(CPM_ERR_ARG, "cpm_apply_sync: null band");
+  if (b->as) {
+    CPM_CUDA(cudaStreamSynchronize(b->as->in));
+    CPM_CUDA(cudaStreamSynchronize(b->as->out));
+  }
+  return CPM_OK;
+}
+
 int cpm_solve(const cpm_band* b, double c, const double* f, double* u, double rtol, int restart,
               int maxit, const cpm_ras* ras, cpm_solve_stats* stats, void* stream);
 

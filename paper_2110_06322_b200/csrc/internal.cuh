@@ -146,6 +146,15 @@ struct cpm_band {
   // host staging for host-pointer calls
   double* dstage0 = nullptr;       // nA
   double* dstage1 = nullptr;       // nA
+  // cpm_apply_async (pinned host buffers): two staging slots, copy-in / copy-out streams
+  struct AsyncStage {
+    double* u[2] = {nullptr, nullptr};
+    double* y[2] = {nullptr, nullptr};
+    cudaStream_t in = nullptr, out = nullptr;
+    cudaEvent_t ein[2] = {nullptr, nullptr}, ek[2] = {nullptr, nullptr}, eout[2] = {nullptr, nullptr};
+    unsigned calls = 0;
+  };
+  AsyncStage* as = nullptr;
   int64_t bytes = 0;
   cpm::Workspace* ws = nullptr;    // cached GMRES workspace (host-owned object)
 };

@@ -380,6 +380,7 @@ int part_create(const cpm_band* B, int rank, int R, cudaStream_t s, cpm_part** o
   CPM_CUDA(cudaMemcpyAsync(L.acell, B->acell + P->lo, sizeof(uint16_t) * P->nOwned,
                            cudaMemcpyDeviceToDevice, s));
   CPM_CUDA(cudaMalloc(&L.vb, sizeof(double) * kBrickCells * (size_t)std::max(nTs, 1)));
+  CPM_CUDA(cudaMemsetAsync(L.vb, 0, sizeof(double) * kBrickCells * (size_t)std::max(nTs, 1), s));
   CPM_CUDA(cudaMalloc(&P->hbuf, sizeof(double) * std::max(nH, 1)));
   CPM_CUDA(cudaGetLastError());
 

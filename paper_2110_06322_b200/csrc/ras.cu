@@ -549,6 +549,7 @@ int ras_setup_device(const cpm_band* B, int S, int overlap, int k, double c, cud
   CPM_CUDA(cudaMalloc(&M.tiles, sizeof(TileHdr) * std::max(nTs, 1)));
   CPM_CUDA(cudaMalloc(&M.acell, sizeof(uint16_t) * std::max<int64_t>(R->ntot, 1)));
   CPM_CUDA(cudaMalloc(&M.vb, sizeof(double) * kBrickCells * (size_t)std::max(nTs, 1)));
+  CPM_CUDA(cudaMemsetAsync(M.vb, 0, sizeof(double) * kBrickCells * (size_t)std::max(nTs, 1), s));
   CPM_CUDA(cudaMalloc(&R->gidx, sizeof(int64_t) * std::max<int64_t>(R->ntot, 1)));
 
   // phase B: per-subdomain structures

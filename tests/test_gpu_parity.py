@@ -385,3 +385,25 @@ def test_full_size_manufactured_solve(cpm, big):
     sel = np.random.default_rng(2).choice(big.n, 500, replace=False)
     fr = f.cpu().numpy()[sel] - apply_rows(_B, c, u_of, ga[sel])
     assert np.abs(fr).max() <= 1e-6 * np.abs(f.cpu().numpy()).max()
+
+
+def test_apply_async_pinned_matches_apply(cpm):
+    """cpm_apply_async on pinned host buffers (pipelined copies, two staging slots)
+    gives the device apply's result for every call of a sequence."""
+    gb = _gpu_band(cpm, "sphere", 0.1)
+    ga = cpm.cpm_band_active_coords(gb).astype(np.int64)
+    us = [torch.from_numpy(seeded_inputs.uniform_pm1(s, ga)).pin_memory() for s in range(5)]
+    ys = [torch.empty(gb.n, dtype=torch.float64).pin_memory() for _ in range(5)]
+    for u, y in zip(us, ys):
+        cpm.cpm_apply_async(gb, 2.0, u.numpy(), y.numpy())
+    cpm.cpm_apply_sync(gb)
+    torch.cuda.synchronize()
+    for u, y in zip(us, ys):
+        yd = torch.empty(gb.n, dtype=torch.float64, device="cuda")
+        cpm.cpm_apply(gb, 2.0, u.cuda(), yd)
+        torch.cuda.synchronize()
+        assert torch.equal(yd.cpu(), y)
+    # pageable host memory falls back to the synchronous cpm_apply
+    yp = np.empty(gb.n)
+    cpm.cpm_apply_async(gb, 2.0, us[0].numpy().copy(), yp)
+    assert np.array_equal(yp, ys[0].numpy())

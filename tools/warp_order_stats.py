@@ -16,13 +16,15 @@ import paper_2110_06322_b200 as cpm
 NT = 128  # threads per extend CTA (apply.cu kNtThreads)
 
 
-def tile_warps(e0, e1, np_, sx, sxy, eoff):
-    """Per warp of the tile: (round k, slot bases [32] or -1, is-single flags)."""
+def tile_warps(e0, e1, npnd, sx, sxy, eoff):
+    """Per warp of the tile: (round k, slot bases [32] or -1, is-single flags).
+    npnd = np | nd << 16 (apply.cu slot_node: pairs, nd duplicated singles, singles)."""
     ne = e1 - e0
+    np_, nd = npnd & 0xFFFF, npnd >> 16
     np2 = 2 * np_
-    nslot = 2 * ne - np2
+    nslot = ne + nd
     s = np.arange(nslot)
-    node = np.where(s < np2, s, np2 + (s - np2) // 2)
+    node = np.where(s < np2, s, np.where(s < np2 + 2 * nd, np2 + (s - np2) // 2, s - nd))
     base = (eoff[e0 + node] & 0xFFFF).astype(np.int64)
     single = s >= np2
     out = []
@@ -110,7 +112,7 @@ def main():
     for t in pick:
         e0, e1, np_, sx, sxy, _ = (int(v) for v in tiles[t])
         if os.environ.get("REDEAL"):
-            sl = redeal(e0, e1, np_, eoff)
+            sl = redeal(e0, e1, np_ & 0xFFFF, eoff)
             ws = [(w0 // NT, np.pad(sl[w0:w0 + 32], (0, max(0, 32 - len(sl[w0:w0 + 32]))),
                                     constant_values=-1), 0.0) for w0 in range(0, len(sl), 32)]
         else:
