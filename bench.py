@@ -114,7 +114,7 @@ KERNELS = ["extend", "laplace", "mdot", "cgs_update", "cgs_final", "axpy", "othe
 
 def _traffic():
     """ncu DRAM bytes (read + write) per apply, from the committed capture summary."""
-    p = os.path.join(ROOT, "profiles", "r01_traffic.json")
+    p = os.path.join(ROOT, "profiles", "r02_traffic.json")
     try:
         d = json.load(open(p))
         return float(d["apply_dram_bytes"])
@@ -462,9 +462,10 @@ def run_mine(args):
                          "alg_bytes_per_apply": alg_bytes,
                          "apply_ms": mean_apply_s * 1e3,
                          "extend_ms": ext_ms / max(ext_n, 1), "laplace_ms": lap_ms / max(lap_n, 1),
-                         "note": "extend is bound by its per-tile load chain overlapped with FP64 and "
-                                 "shared-memory gathers (DESIGN.md §Kernels, ablations); "
-                                 "traffic = ncu DRAM bytes per apply (profiles/r01_traffic.json)"},
+                         "note": "the extend is bound by its l1tex issue (64 shared-memory gathers per node "
+                                 "slot, the cp.async box fill, scattered E u stores: DESIGN.md §Kernels, "
+                                 "profiles/r02_extend_sass_l1tex.txt); traffic = ncu DRAM bytes per apply "
+                                 "(profiles/r02_traffic.json)"},
             "roofline_solve": {"kernel": "Krylov passes of the solve (k_dcgs_dots + k_dcgs_update), "
                                          "the largest share of a step",
                                "bound": "hbm", "achieved": kry_gbs, "peak": peak, "unit": "GB/s",

@@ -601,8 +601,10 @@ static __global__ void __launch_bounds__(256, MINB) k_dcgs_dots_direct(
   const int64_t stride = (int64_t)S.gps * TE;
   // UN tiles per iteration (all their loads issued before the FMAs); per lane the
   // tiles are still summed in increasing order
-  for (int64_t tb = (int64_t)lb * TE; tb < n; tb += (UN > 0 ? UN : 1) * stride) {
-    constexpr int UQ = UN > 0 ? UN : 1;
+  // UN > 0: UN tiles per iteration, one column's loads at a time; UN <= 0: max(1, -UN)
+  // tiles per iteration with every owned column's loads issued before the FMAs
+  constexpr int UQ = UN > 0 ? UN : (UN == 0 ? 1 : -UN);
+  for (int64_t tb = (int64_t)lb * TE; tb < n; tb += UQ * stride) {
     double u[UQ][4], zv[UQ][4];
 #pragma unroll
     for (int q = 0; q < UQ; ++q) {
@@ -620,29 +622,35 @@ static __global__ void __launch_bounds__(256, MINB) k_dcgs_dots_direct(
         zv[q][2] = e1 < n ? __ldg(zz + e1) : 0.0; zv[q][3] = e1 + 1 < n ? __ldg(zz + e1 + 1) : 0.0;
       }
     }
-    if (UN == 0) {  // one tile, every owned column's loads issued before the FMAs
-      const int64_t e0 = tb + 2 * lane, e1 = tb + 64 + 2 * lane;
-      const bool fv = tb + TE <= n && vec2;
-      double v[KW][4];
+    if (UN <= 0) {  // every owned column's loads of the UQ tiles issued before the FMAs
+      double v[UQ][KW][4];
 #pragma unroll
-      for (int c = 0; c < KW; ++c) {
-        const int i = warp + c * NW;
-        const double* col = V + (size_t)min(i, k - 1) * ldv + o0;
-        if (fv) {
-          const double2 va = __ldcs((const double2*)(col + e0)), vb = __ldcs((const double2*)(col + e1));
-          v[c][0] = va.x; v[c][1] = va.y; v[c][2] = vb.x; v[c][3] = vb.y;
-        } else {
-          v[c][0] = e0 < n ? __ldcs(col + e0) : 0.0; v[c][1] = e0 + 1 < n ? __ldcs(col + e0 + 1) : 0.0;
-          v[c][2] = e1 < n ? __ldcs(col + e1) : 0.0; v[c][3] = e1 + 1 < n ? __ldcs(col + e1 + 1) : 0.0;
+      for (int q = 0; q < UQ; ++q) {
+        const int64_t t0 = tb + q * stride;
+        const int64_t e0 = t0 + 2 * lane, e1 = t0 + 64 + 2 * lane;
+        const bool fv = t0 + TE <= n && vec2;
+#pragma unroll
+        for (int c = 0; c < KW; ++c) {
+          const int i = warp + c * NW;
+          const double* col = V + (size_t)min(i, k - 1) * ldv + o0;
+          if (fv) {
+            const double2 va = __ldcs((const double2*)(col + e0)), vb = __ldcs((const double2*)(col + e1));
+            v[q][c][0] = va.x; v[q][c][1] = va.y; v[q][c][2] = vb.x; v[q][c][3] = vb.y;
+          } else {
+            v[q][c][0] = e0 < n ? __ldcs(col + e0) : 0.0; v[q][c][1] = e0 + 1 < n ? __ldcs(col + e0 + 1) : 0.0;
+            v[q][c][2] = e1 < n ? __ldcs(col + e1) : 0.0; v[q][c][3] = e1 + 1 < n ? __ldcs(col + e1 + 1) : 0.0;
+          }
         }
       }
 #pragma unroll
-      for (int c = 0; c < KW; ++c)
+      for (int q = 0; q < UQ; ++q)
 #pragma unroll
-        for (int x = 0; x < 4; ++x) {
-          a1[c] = fma(v[c][x], u[0][x], a1[c]);
-          a2[c] = fma(v[c][x], zv[0][x], a2[c]);
-        }
+        for (int c = 0; c < KW; ++c)
+#pragma unroll
+          for (int x = 0; x < 4; ++x) {
+            a1[c] = fma(v[q][c][x], u[q][x], a1[c]);
+            a2[c] = fma(v[q][c][x], zv[q][x], a2[c]);
+          }
       continue;
     }
 #pragma unroll
@@ -995,7 +1003,17 @@ inline int launch_dcgs_dots_epi(const vec::Seg& S, int k, const double* V, int64
   const bool direct = direct_env && S.nseg == 1;
   // register-direct reduction pass: every owned column's loads of a tile issued
   // before its FMAs (UN = 0), columns per warp KW by k (fewer registers for small k)
-  if (direct && k <= 8 * 2) {
+  static const int tt = [] {  // CPM_DOTS_TT=1: one tile per iteration also for k <= 32 (A/B)
+    const char* v = getenv("CPM_DOTS_TT");
+    return v ? atoi(v) : 2;
+  }();
+  if (direct && k <= 8 * 2 && tt == 2) {
+    CPM_CUDA(launch_pdl(vec::k_dcgs_dots_direct<2, 2, -3, Epi>, dim3(grid), dim3(256), 0, st, S, k, V, ldv, z,
+                        partial, pld, out, ldo, counters, skip, epi));
+  } else if (direct && k <= 8 * 4 && tt == 2) {
+    CPM_CUDA(launch_pdl(vec::k_dcgs_dots_direct<4, 2, -2, Epi>, dim3(grid), dim3(256), 0, st, S, k, V, ldv, z,
+                        partial, pld, out, ldo, counters, skip, epi));
+  } else if (direct && k <= 8 * 2) {
     CPM_CUDA(launch_pdl(vec::k_dcgs_dots_direct<2, 2, 0, Epi>, dim3(grid), dim3(256), 0, st, S, k, V, ldv, z,
                         partial, pld, out, ldo, counters, skip, epi));
   } else if (direct && k <= 8 * 4) {
