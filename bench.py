@@ -766,8 +766,8 @@ def main():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     if "WORLD_SIZE" not in os.environ and args.gpus > 1:
         return _self_launch(args)
-    if ws > 1:
-        return run_partitioned(args)
+    if ws > 1 or (os.environ.get("CPM_BENCH_PARTITIONED") == "1" and "WORLD_SIZE" in os.environ):
+        return run_partitioned(args)  # (the env switch runs this path with one rank, as a check)
     return run_mine(args)
 
 
