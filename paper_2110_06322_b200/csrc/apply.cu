@@ -334,6 +334,104 @@ __global__ void __launch_bounds__(kLapThreads) k_laplace(const TileHdr* __restri
 }
 
 
+// ------------------------------------------------------------------ fused apply (experiment)
+// One CTA (128 threads) per tile, no vb: stage the FUSED box (build.cu build_fused:
+// the stencils of the tile's eval nodes and of its halo nodes, the face-neighbour
+// eval nodes next to its active nodes), contract the own eval nodes (pair order of
+// k_extend_nt) and the halo nodes into the dense 10^3 halo brick in shared memory,
+// then the 7-point combination for the tile's output nodes.  E u never leaves the SM;
+// the price is the halo nodes' second evaluation.
+__device__ __forceinline__ double contract_val(double tnx, double tny, double tnz, const double* __restrict__ p,
+                                               int sx, int sxy) {
+  double wx[4], wy[4], wz[4];
+  lagrange4(tnx, wx);
+  lagrange4(tny, wy);
+  lagrange4(tnz, wz);
+  double acc = 0.0;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    double accy = 0.0;
+#pragma unroll
+    for (int bb = 0; bb < 4; ++bb) {
+      const double* row = p + bb * sx + c * sxy;
+      const double rx = (wx[0] * row[0] + wx[1] * row[1]) + (wx[2] * row[2] + wx[3] * row[3]);
+      accy += wy[bb] * rx;
+    }
+    acc += wz[c] * accy;
+  }
+  return acc;
+}
+
+__global__ void __launch_bounds__(kNtThreads, 6)
+    k_apply_fused(const TileHdr* __restrict__ ftiles, int boxCells, int descCap, const uint64_t* __restrict__ runs,
+                  const double* __restrict__ u, const double* __restrict__ tx, const double* __restrict__ ty,
+                  const double* __restrict__ tz, const uint32_t* __restrict__ feoff, const int* __restrict__ hst,
+                  const uint64_t* __restrict__ halo, const uint16_t* __restrict__ acell, double* __restrict__ y,
+                  double diag, double ih2, const double* __restrict__ scale, int lds, const int* __restrict__ skip) {
+  extern __shared__ double smf[];
+  double* box = smf;
+  uint64_t* desc = (uint64_t*)(box + boxCells);
+  __shared__ double E[1000];
+  const int t = blockIdx.x, tid = threadIdx.x;
+  const TileHdr* T = ftiles + t;
+  const int e0 = T->e0, ne = T->e1 - e0, r0 = T->r0, r1 = T->r1;
+  const int np2 = 2 * T->np, nd = T->pad2, nslot = ne + nd;
+  const int sx = T->pad[0], sxy = T->pad[1];
+  const int h0 = hst[t], nh = hst[t + 1] - h0;
+  const int a0 = T->a0, a1 = T->a1;
+  const int g = tid >> 3, l = tid & 7;
+  int nr = min(descCap, r1 - r0);
+  for (int r = tid; r < nr; r += kNtThreads) cp_async8_hint(desc + r, runs + r0 + r, policy_evict_first());
+  cp_commit();
+  pdl_wait();
+  if (skip && *skip) {
+    cp_wait<0>();
+    return;
+  }
+  const uint64_t plast = policy_evict_last();
+  for (int c0 = r0; c0 < r1; c0 += nr, nr = min(descCap, r1 - c0)) {
+    if (c0 > r0) {
+      __syncthreads();
+      for (int r = tid; r < nr; r += kNtThreads) cp_async8_hint(desc + r, runs + c0 + r, policy_evict_first());
+      cp_commit();
+    }
+    cp_wait<0>();
+    __syncthreads();
+    for (int r = g; r < nr; r += kNtThreads / 8) {
+      const uint64_t d = desc[r];
+      const uint32_t src = (uint32_t)d, dst = (uint32_t)(d >> 32) & 0xffffu, len = (uint32_t)(d >> 48) & 0xffu;
+      if (l < len) cp_async8_hint(box + dst + l, u + src + l, plast);
+    }
+    cp_commit();
+  }
+  cp_wait<0>();
+  __syncthreads();
+  // own eval nodes (k_extend_nt's slot order) -> E at their brick cells
+  for (int sl = tid; sl < nslot; sl += kNtThreads) {
+    bool w;
+    const int i = e0 + slot_node(sl, np2, nd, w);
+    const uint32_t eo = __ldg(feoff + i);
+    const double v = contract_val(__ldg(tx + i), __ldg(ty + i), __ldg(tz + i), box + (eo & 0xffffu), sx, sxy);
+    const int c = (int)(eo >> 16);
+    if (w) E[hidx(c & 7, (c >> 3) & 7, c >> 6)] = v;
+  }
+  // halo nodes (the neighbours' eval nodes next to own active nodes) -> E halo layer
+  for (int k = tid; k < nh; k += kNtThreads) {
+    const uint64_t hv = __ldg(halo + h0 + k);
+    const int i = (int)(uint32_t)hv;
+    const uint32_t off = (uint32_t)(hv >> 32) & 0xffffu;
+    E[(int)(hv >> 48)] = contract_val(__ldg(tx + i), __ldg(ty + i), __ldg(tz + i), box + off, sx, sxy);
+  }
+  __syncthreads();
+  const double s = scale ? __ldg(scale + (size_t)T->pad[2] * lds) : 1.0;
+  for (int a = a0 + tid; a < a1; a += kNtThreads) {
+    const int c = __ldg(acell + a);
+    const int h = hidx(c & 7, (c >> 3) & 7, c >> 6);
+    const double sum = E[h + 1] + E[h - 1] + E[h + 10] + E[h - 10] + E[h + 100] + E[h - 100];
+    y[a] = s * (diag * __ldg(u + a) - ih2 * sum);
+  }
+}
+
 }  // namespace
 
 int apply_device(const cpm_band* b, double c, const double* u, double* y, const double* scale,
@@ -402,6 +500,25 @@ int laplace_tiles(const cpm_band* b, double c, const double* u, double* y, const
 int apply_device_split(const cpm_band* b, double c, const double* u, const double* uh, double* y,
                        const double* scale, int lds, cudaStream_t s, const int* skip) {
   if (b->nT == 0) return CPM_OK;  // no tiles (an empty sub-band): nothing to write
+  if (b->fzT) {  // the fused single-kernel apply (bands built with CPM_FUSED=1)
+    const double ih2 = 1.0 / (b->h * b->h);
+    const int descCap = 512;
+    const size_t smem = (size_t)b->fzMaxBox * 8 + (size_t)descCap * 8;
+    static bool attr = false;
+    if (!attr) {
+      CPM_CUDA(cudaFuncSetAttribute(k_apply_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      attr = true;
+    }
+    ProfScope ps(K_EXTEND, s);
+    CPM_CUDA(launch_pdl(k_apply_fused, dim3((unsigned)b->nT), dim3(kNtThreads), smem, s, (const TileHdr*)b->fzT,
+                        b->fzMaxBox, descCap, (const uint64_t*)b->fzRuns, u, (const double*)b->tx,
+                        (const double*)b->ty, (const double*)b->tz, (const uint32_t*)b->fzEoff,
+                        (const int*)b->fzH, (const uint64_t*)b->fzHalo, (const uint16_t*)b->acell, y,
+                        c + 6.0 * ih2, ih2, scale, lds, skip));
+    count_launch();
+    CPM_CUDA(cudaGetLastError());
+    return CPM_OK;
+  }
   CPM_TRY(extend_tiles(b, u, uh, s, skip, 0, b->nT));
   return laplace_tiles(b, c, u, y, scale, lds, s, skip);
 }

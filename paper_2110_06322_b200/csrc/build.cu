@@ -645,6 +645,159 @@ __global__ void k_flags(int nb, const int* ne, int* flag) {
   if (b == 0) flag[nb] = 0;
 }
 
+// ------------------------------------------------------------------ F (fused-apply experiment)
+// For the single-kernel apply (apply.cu k_apply_fused): every tile also evaluates
+// E u at its HALO nodes — the eval nodes of face-neighbour tiles that are 6-neighbours
+// of its own active nodes — so no E u crosses HBM.  Its box must cover the halo
+// nodes' stencils too (the "fused box"); the own nodes keep their order (pairs).
+// Bases are decoded from the final box offsets (the eval order was permuted).
+__device__ inline void decode_base(const TileHdr& T, uint32_t eo, int* b) {
+  const int o = (int)(eo & 0xffffu);
+  const int dz = o / T.pad[1], rem = o - dz * T.pad[1], dy = rem / T.pad[0], dx = rem - dy * T.pad[0];
+  b[0] = T.ox + dx;
+  b[1] = T.oy + dy;
+  b[2] = T.oz + dz;
+}
+
+// cell -> local eval index of every tile (0xffff: not an eval cell)
+__global__ void k_fz_cmap(const TileHdr* tiles, const uint32_t* eoff, uint16_t* cmap) {
+  const int t = blockIdx.x;
+  const TileHdr T = tiles[t];
+  for (int c = threadIdx.x; c < 512; c += blockDim.x) cmap[(size_t)t * 512 + c] = 0xffffu;
+  __syncthreads();
+  for (int e = T.e0 + threadIdx.x; e < T.e1; e += blockDim.x)
+    cmap[(size_t)t * 512 + (eoff[e] >> 16)] = (uint16_t)(e - T.e0);
+}
+
+// halo nodes of tile t: face f, face cell (i, j): own boundary cell active and the
+// neighbour's facing cell an eval cell.  WRITE = false counts, true fills.
+template <bool WRITE>
+__global__ void k_fz_halo(const TileHdr* tiles, const uint32_t* tam, const uint16_t* cmap, int* cnt,
+                          const int* hstart, uint64_t* halo) {
+  const int t = blockIdx.x, q = threadIdx.x;  // 384 threads: f = q / 64
+  __shared__ int n;
+  if (q == 0) n = 0;
+  __syncthreads();
+  const TileHdr T = tiles[t];
+  const int f = q >> 6, i = q & 7, j = (q >> 3) & 7;
+  const int src = T.nbr[f];
+  bool take = false;
+  int c = 0, h = 0;
+  if (src >= 0) {
+    const int axis = f >> 1, plus = (f & 1) == 0;
+    const int in = plus ? 0 : 7, me = plus ? 7 : 0, out = plus ? 8 : -1;
+    int co;
+    if (axis == 0) { c = in + 8 * i + 64 * j; co = me + 8 * i + 64 * j; h = (out + 1) + 10 * (i + 1) + 100 * (j + 1); }
+    else if (axis == 1) { c = i + 8 * in + 64 * j; co = i + 8 * me + 64 * j; h = (i + 1) + 10 * (out + 1) + 100 * (j + 1); }
+    else { c = i + 8 * j + 64 * in; co = i + 8 * j + 64 * me; h = (i + 1) + 10 * (j + 1) + 100 * (out + 1); }
+    take = mask_has(tam + (size_t)t * 16, co) && cmap[(size_t)src * 512 + c] != 0xffffu;
+  }
+  if (take) {
+    const int k = atomicAdd(&n, 1);
+    if (WRITE) {
+      const uint32_t e = (uint32_t)(tiles[src].e0 + cmap[(size_t)src * 512 + c]);
+      halo[hstart[t] + k] = (uint64_t)e | ((uint64_t)h << 48);
+    }
+  }
+  __syncthreads();
+  if (!WRITE && q == 0) cnt[t] = n;
+}
+
+// the union of own and halo stencil bases per tile into ub (tile t at e0 + hstart[t] ..),
+// and the temp header ft with that range; bbox + strides of the fused box
+__global__ void __launch_bounds__(256) k_fz_box(int nT, const TileHdr* tiles, const uint32_t* eoff,
+                                                const int* hstart, const uint64_t* halo, int32_t* ub,
+                                                TileHdr* ft, int* err, int* maxbox) {
+  const int t = blockIdx.x;
+  TileHdr T = tiles[t];
+  const int ne = T.e1 - T.e0, h0 = hstart[t], nh = hstart[t + 1] - h0, u0 = T.e0 + h0;
+  int lo[3] = {INT_MAX, INT_MAX, INT_MAX}, hi[3] = {INT_MIN, INT_MIN, INT_MIN};
+  for (int k = threadIdx.x; k < ne + nh; k += blockDim.x) {
+    int b[3];
+    if (k < ne) {
+      decode_base(T, eoff[T.e0 + k], b);
+    } else {
+      const uint64_t hv = halo[h0 + k - ne];
+      const uint32_t e = (uint32_t)hv;
+      // the node's own tile: found through the eval ranges (binary search)
+      int l = 0, r = nT - 1;
+      while (l < r) {
+        const int m = (l + r + 1) >> 1;
+        if (tiles[m].e0 <= (int)e) l = m; else r = m - 1;
+      }
+      decode_base(tiles[l], eoff[e], b);
+    }
+    for (int q = 0; q < 3; ++q) {
+      ub[3 * (size_t)(u0 + k) + q] = b[q];
+      lo[q] = min(lo[q], b[q]);
+      hi[q] = max(hi[q], b[q]);
+    }
+  }
+  using BR = cub::BlockReduce<int, 256>;
+  __shared__ typename BR::TempStorage tmp;
+  __shared__ int res[6];
+  for (int q = 0; q < 3; ++q) {
+    const int a = BR(tmp).Reduce(lo[q], cub::Min());
+    __syncthreads();
+    const int b = BR(tmp).Reduce(hi[q], cub::Max());
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      res[q] = a;
+      res[3 + q] = b;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    T.ox = res[0];
+    T.oy = res[1];
+    T.oz = res[2];
+    T.sx = res[3] - res[0] + 4;
+    T.sy = res[4] - res[1] + 4;
+    T.sz = res[5] - res[2] + 4;
+    // the same stride rule as k_tile_box (small neighbour offsets in distinct banks)
+    int best = INT_MAX, bpx = T.sx, bpxy = T.sx * T.sy;
+    for (int dx = 0; dx < 16; ++dx)
+      for (int dz = 0; dz < 16; ++dz) {
+        const int px = T.sx + dx, pxy = px * T.sy + dz;
+        const int d[9] = {1, px, pxy, px + 1, px - 1, pxy + 1, pxy - 1, pxy + px, pxy - px};
+        int score = 0;
+        for (int a = 0; a < 9; ++a) {
+          if ((d[a] & 15) == 0) score += 16;
+          for (int b = a + 1; b < 9; ++b)
+            if (((d[a] - d[b]) & 15) == 0) score += 1;
+        }
+        score = score * 100000 + pxy * T.sz;
+        if (score < best) {
+          best = score;
+          bpx = px;
+          bpxy = pxy;
+        }
+      }
+    T.pad[0] = bpx;
+    T.pad[1] = bpxy;
+    const int cells = bpxy * T.sz;
+    if (T.sx > kMaxBoxEdge || T.sy > kMaxBoxEdge || T.sz > kMaxBoxEdge || cells > kMaxBoxCells) atomicOr(err, 1);
+    atomicMax(maxbox, cells);
+    T.e0 = u0;  // the temp header's node range: into ub
+    T.e1 = u0 + ne + nh;
+    ft[t] = T;
+  }
+}
+
+// fused-box offsets of the own nodes and the halo nodes
+__global__ void k_fz_offsets(const TileHdr* tiles, const TileHdr* ft, const int* hstart, const int32_t* ub,
+                             const uint32_t* eoff, uint32_t* fzeoff, uint64_t* halo) {
+  const int t = blockIdx.x;
+  const TileHdr T = tiles[t], F = ft[t];
+  const int ne = T.e1 - T.e0, h0 = hstart[t], nh = hstart[t + 1] - h0;
+  for (int k = threadIdx.x; k < ne + nh; k += blockDim.x) {
+    const int32_t* b = ub + 3 * (size_t)(F.e0 + k);
+    const uint32_t off = (uint32_t)((b[0] - F.ox) + F.pad[0] * (b[1] - F.oy) + F.pad[1] * (b[2] - F.oz));
+    if (k < ne) fzeoff[T.e0 + k] = off | (eoff[T.e0 + k] & 0xffff0000u);
+    else halo[h0 + k - ne] |= (uint64_t)off << 32;
+  }
+}
+
 // ------------------------------------------------------------------ host helpers
 struct DevBuf {
   void* p = nullptr;
@@ -701,6 +854,74 @@ int read_back(const T* dptr, T* hval, cudaStream_t s) {
 
 inline int grid_for(int64_t n, int bs) { return (int)std::max<int64_t>(1, std::min<int64_t>((n + bs - 1) / bs, 1 << 30)); }
 
+__global__ void k_fz_restore(int nT, const TileHdr* tiles, TileHdr* ft) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < nT) {  // back to the eval-node range (the runs were built over the ub range)
+    ft[t].e0 = tiles[t].e0;
+    ft[t].e1 = tiles[t].e1;
+  }
+}
+
+int build_fused(cpm_band* B, const int* bmap, const int* dblo, const int* dbdim, cudaStream_t s) {
+  const int nT = B->nT;
+  DevBuf cmap, cnt, hst, ftb, ub, err;
+  CPM_TRY(dalloc<uint16_t>(cmap, (size_t)nT * 512, "fz cmap"));
+  CPM_TRY(dalloc<int>(cnt, nT + 1, "fz cnt"));
+  CPM_TRY(dalloc<int>(err, 2, "fz err"));
+  CPM_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(int) * (nT + 1), s));
+  CPM_CUDA(cudaMemsetAsync(err.p, 0, sizeof(int) * 2, s));
+  k_fz_cmap<<<nT, 256, 0, s>>>(B->tiles, B->eoff, cmap.as<uint16_t>());
+  k_fz_halo<false><<<nT, 384, 0, s>>>(B->tiles, B->amask, cmap.as<uint16_t>(), cnt.as<int>(), nullptr, nullptr);
+  CPM_TRY(dalloc_owned(&B->fzH, (size_t)nT + 1, &B->bytes, "fz hstart"));
+  CPM_TRY(exclusive_sum(cnt.as<int>(), B->fzH, nT + 1, s));
+  int nH = 0;
+  CPM_TRY(read_back(B->fzH + nT, &nH, s));
+  B->fzNHalo = nH;
+  CPM_TRY(dalloc_owned(&B->fzHalo, (size_t)std::max(nH, 1), &B->bytes, "fz halo"));
+  k_fz_halo<true><<<nT, 384, 0, s>>>(B->tiles, B->amask, cmap.as<uint16_t>(), nullptr, B->fzH, B->fzHalo);
+  // note: the halo list order inside a tile is atomic-order (any order is correct)
+  CPM_TRY(dalloc<TileHdr>(ftb, nT, "fz tiles"));
+  CPM_TRY(dalloc<int32_t>(ub, 3 * ((size_t)B->nE + 8 + (size_t)nH), "fz bases"));
+  k_fz_box<<<nT, 256, 0, s>>>(nT, B->tiles, B->eoff, B->fzH, B->fzHalo, ub.as<int32_t>(), ftb.as<TileHdr>(),
+                              err.as<int>(), err.as<int>() + 1);
+  CPM_TRY(dalloc_owned(&B->fzEoff, (size_t)B->nE + 8, &B->bytes, "fz eoff"));
+  k_fz_offsets<<<nT, 256, 0, s>>>(B->tiles, ftb.as<TileHdr>(), B->fzH, ub.as<int32_t>(), B->eoff, B->fzEoff,
+                                  B->fzHalo);
+  int herr[2] = {0, 0};
+  CPM_CUDA(cudaMemcpyAsync(herr, err.p, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
+  CPM_CUDA(cudaStreamSynchronize(s));
+  if (herr[0]) return fail(CPM_ERR_LIMIT, "fused apply: a fused stencil box exceeds the limit");
+  B->fzMaxBox = herr[1];
+  // fill runs of the fused boxes (k_runs over the own + halo bases)
+  DevBuf nrows, rowbase, rowcnt, runstart;
+  CPM_TRY(dalloc<int64_t>(nrows, nT + 1, "fz nrows"));
+  CPM_TRY(dalloc<int64_t>(rowbase, nT + 1, "fz rowbase"));
+  k_rows_per_tile<<<grid_for(nT + 1, 256), 256, 0, s>>>(nT, ftb.as<TileHdr>(), nrows.as<int64_t>());
+  CPM_TRY(exclusive_sum(nrows.as<int64_t>(), rowbase.as<int64_t>(), nT + 1, s));
+  int64_t totRows = 0;
+  CPM_TRY(read_back(rowbase.as<int64_t>() + nT, &totRows, s));
+  CPM_TRY(dalloc<int64_t>(rowcnt, totRows + 1, "fz rowcnt"));
+  CPM_TRY(dalloc<int64_t>(runstart, totRows + 1, "fz runstart"));
+  CPM_CUDA(cudaMemsetAsync(rowcnt.p, 0, (totRows + 1) * sizeof(int64_t), s));
+  k_runs<false><<<nT, 128, 0, s>>>(ftb.as<TileHdr>(), ub.as<int32_t>(), B->amask, bmap, dblo, dbdim,
+                                   rowbase.as<int64_t>(), rowcnt.as<int64_t>(), nullptr, nullptr);
+  CPM_TRY(exclusive_sum(rowcnt.as<int64_t>(), runstart.as<int64_t>(), totRows + 1, s));
+  int64_t totRuns = 0;
+  CPM_TRY(read_back(runstart.as<int64_t>() + totRows, &totRuns, s));
+  CPM_TRY(dalloc_owned(&B->fzRuns, (size_t)totRuns + 2, &B->bytes, "fz runs"));
+  k_runs<true><<<nT, 128, 0, s>>>(ftb.as<TileHdr>(), ub.as<int32_t>(), B->amask, bmap, dblo, dbdim,
+                                  rowbase.as<int64_t>(), rowcnt.as<int64_t>(), runstart.as<int64_t>(), B->fzRuns);
+  k_set_run_ranges<<<grid_for(nT, 256), 256, 0, s>>>(nT, ftb.as<TileHdr>(), rowbase.as<int64_t>(),
+                                                      runstart.as<int64_t>());
+  B->fzNRuns = totRuns;
+  k_fz_restore<<<grid_for(nT, 256), 256, 0, s>>>(nT, B->tiles, ftb.as<TileHdr>());
+  CPM_TRY(dalloc_owned(&B->fzT, (size_t)nT, &B->bytes, "fz tiles"));
+  CPM_CUDA(cudaMemcpyAsync(B->fzT, ftb.p, sizeof(TileHdr) * nT, cudaMemcpyDeviceToDevice, s));
+  CPM_CUDA(cudaGetLastError());
+  CPM_CUDA(cudaStreamSynchronize(s));
+  return CPM_OK;
+}
+
 }  // namespace
 
 void free_workspace(Workspace* w);
@@ -724,7 +945,7 @@ void free_band(cpm_band* b) {
   if (b->owns) {
     void* ptrs[] = {b->tiles, b->tx,      b->ty,      b->tz,    b->eoff, b->acell,
                     b->aijk,  b->gijk,    b->runs,    b->vb,    b->dstage0, b->dstage1,
-                    b->amask, b->bmap};
+                    b->amask, b->bmap,    b->fzT,     b->fzH,   b->fzHalo, b->fzEoff, b->fzRuns};
     for (void* p : ptrs)
       if (p) cudaFree(p);
   } else {  // sub-band: owns only its own tiles/runs/acell/vb
@@ -972,6 +1193,8 @@ int build_band(const cpm_surface* surf, double h, int p, double L, cudaStream_t 
   CPM_CUDA(cudaGetLastError());
   B->nRuns = totRuns;
 
+  if (getenv("CPM_FUSED") && *getenv("CPM_FUSED") == '1')
+    CPM_TRY(build_fused(B, bmap.as<int>(), dblo.as<int>(), dbdim.as<int>(), s));
   CPM_TRY(dalloc_owned(&B->vb, (size_t)totT * kBrickCells, &B->bytes, "vb"));
   // cells outside Sigma_A u Sigma_G are never written by the extend; k_laplace loads
   // whole slots (never using those cells): defined values for them

@@ -157,6 +157,16 @@ struct cpm_band {
   AsyncStage* as = nullptr;
   int64_t bytes = 0;
   cpm::Workspace* ws = nullptr;    // cached GMRES workspace (host-owned object)
+
+  // single-kernel (fused) apply, an experiment built when CPM_FUSED=1 at band build
+  // (build.cu build_fused, apply.cu k_apply_fused)
+  cpm::TileHdr* fzT = nullptr;     // per tile: the fused box (origin, extents, strides, runs)
+  int* fzH = nullptr;              // nT + 1: halo node ranges
+  uint64_t* fzHalo = nullptr;      // halo nodes: eval index | box offset << 32 | halo cell << 48
+  uint32_t* fzEoff = nullptr;      // own eval nodes: fused box offset | cell << 16
+  uint64_t* fzRuns = nullptr;
+  int fzMaxBox = 0;
+  int64_t fzNHalo = 0, fzNRuns = 0;
 };
 
 namespace cpm {

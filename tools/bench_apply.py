@@ -44,7 +44,7 @@ for K in ks:
     l, _ = cpm.cpm_profile_read("laplace")
     nA, nG = band.info.n_active, band.info.n_ghost
     alg = 16 * nA + 28 * (nA + nG)
-    print(f"K={K} nA={nA} tiles={band.info.n_tiles} runs={band.info.n_runs} maxbox={band.info.max_box} "
+    print(f"{'FUSED ' if os.environ.get('CPM_FUSED') == '1' else ''}K={K} nA={nA} tiles={band.info.n_tiles} runs={band.info.n_runs} maxbox={band.info.max_box} "
           f"apply {ms*1e3:.1f} us (extend {e/N*1e3:.1f} us, laplace {l/N*1e3:.1f} us) -> "
           f"{alg/ms/1e6:.0f} GB/s alg, {nA/ms/1e6:.2f} Gnodes/s, diff vs first K {err:.1e}", flush=True)
     del band
