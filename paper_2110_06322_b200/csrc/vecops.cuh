@@ -581,6 +581,114 @@ static __global__ void __launch_bounds__(256) k_dcgs_dots_bulk(Seg S, int k, con
 // tile's u_j and z (L1 hits after the first warp).  Fixed association order: per
 // lane the tiles in order, then the warp shuffle tree, then the blocks in index
 // order (the last block of the segment, as k_dcgs_dots).  KW = max columns per warp.
+// ---- TMA-staged variant with warp-owned columns (single 16-byte aligned segment):
+// tiles of 128 elements; one thread arms an mbarrier and issues one cp.async.bulk
+// per column (Q_0 .. Q_{k-1} (the last is u_j), z) into a ring of ns stages, so up
+// to ns tiles' columns are in flight without occupying registers; warp w reduces
+// its columns w, w+8, ... of a staged tile with 16-byte shared loads (lane l:
+// elements 2l, 2l+1, 64+2l, 65+2l), u_j and z of the tile held in registers.
+// Same per-lane element order and epilogue as k_dcgs_dots_direct.
+template <int KW, class Epi = NoEpi>
+static __global__ void __launch_bounds__(256, 2) k_dcgs_dots_tma(Seg S, int k, const double* __restrict__ V,
+                                                                  int64_t ldv, const double* __restrict__ z,
+                                                                  double* partial, int pld, double* out, int ldo,
+                                                                  unsigned* counters, const int* __restrict__ skip,
+                                                                  int ns, Epi epi = Epi()) {
+  constexpr int TB = 256, NW = TB / 32, TE = 128;
+  pdl_wait();
+  if (skip && *skip) return;
+  extern __shared__ __align__(16) double smt[];
+  __shared__ __align__(8) uint64_t full[8];
+  __shared__ bool last;
+  const int s = blockIdx.x / S.gps, lb = blockIdx.x % S.gps;
+  const int64_t o0 = S.off[s], n = S.off[s + 1] - o0;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const size_t stage = (size_t)(k + 1) * TE;
+  const int64_t stride = (int64_t)S.gps * TE;
+  if (tid == 0) {
+    for (int q = 0; q < ns; ++q) mbar_init(&full[q], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int64_t t0, int q) {  // thread 0
+    if (t0 >= n) return;
+    const unsigned bytes = (unsigned)((min((int64_t)TE, n - t0) + 1) & ~1) * 8u;  // 16-byte granules
+    double* dst = smt + (size_t)q * stage;
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    mbar_expect_tx(&full[q], bytes * (unsigned)(k + 1));
+    for (int i = 0; i < k; ++i) bulk_g2s(dst + (size_t)i * TE, V + (size_t)i * ldv + o0 + t0, bytes, &full[q]);
+    bulk_g2s(dst + (size_t)k * TE, z + o0 + t0, bytes, &full[q]);
+  };
+  const int64_t tfirst = (int64_t)lb * TE;
+  if (tid == 0)
+    for (int q = 0; q < ns - 1; ++q) issue(tfirst + q * stride, q);
+  double a1[KW], a2[KW];
+#pragma unroll
+  for (int c = 0; c < KW; ++c) a1[c] = a2[c] = 0.0;
+  unsigned ph = 0;
+  int it = 0;
+  for (int64_t t0 = tfirst; t0 < n; t0 += stride, ++it) {
+    const int q = it % ns;
+    if (tid == 0) issue(t0 + (int64_t)(ns - 1) * stride, (it + ns - 1) % ns);
+    mbar_wait(&full[q], (ph >> q) & 1u);
+    ph ^= 1u << q;
+    const double* sv = smt + (size_t)q * stage;
+    const int e0 = 2 * lane, e1 = 64 + 2 * lane;
+    const bool ok0 = t0 + e0 < n, ok1 = t0 + e0 + 1 < n, ok2 = t0 + e1 < n, ok3 = t0 + e1 + 1 < n;
+    const double2 ua = *(const double2*)(sv + (size_t)(k - 1) * TE + e0), ub = *(const double2*)(sv + (size_t)(k - 1) * TE + e1);
+    const double2 za = *(const double2*)(sv + (size_t)k * TE + e0), zb = *(const double2*)(sv + (size_t)k * TE + e1);
+    const double u0 = ok0 ? ua.x : 0.0, u1 = ok1 ? ua.y : 0.0, u2 = ok2 ? ub.x : 0.0, u3 = ok3 ? ub.y : 0.0;
+    const double z0 = ok0 ? za.x : 0.0, z1 = ok1 ? za.y : 0.0, z2 = ok2 ? zb.x : 0.0, z3 = ok3 ? zb.y : 0.0;
+#pragma unroll
+    for (int c = 0; c < KW; ++c) {
+      const int i = warp + c * NW;
+      if (i < k) {
+        const double2 va = *(const double2*)(sv + (size_t)i * TE + e0), vb = *(const double2*)(sv + (size_t)i * TE + e1);
+        const double v0 = ok0 ? va.x : 0.0, v1 = ok1 ? va.y : 0.0, v2 = ok2 ? vb.x : 0.0, v3 = ok3 ? vb.y : 0.0;
+        a1[c] = fma(v0, u0, a1[c]); a2[c] = fma(v0, z0, a2[c]);
+        a1[c] = fma(v1, u1, a1[c]); a2[c] = fma(v1, z1, a2[c]);
+        a1[c] = fma(v2, u2, a1[c]); a2[c] = fma(v2, z2, a2[c]);
+        a1[c] = fma(v3, u3, a1[c]); a2[c] = fma(v3, z3, a2[c]);
+      }
+    }
+    __syncthreads();  // the stage is refilled by the next issue
+  }
+#pragma unroll
+  for (int c = 0; c < KW; ++c) {
+    const int i = warp + c * NW;
+    if (i < k) {
+      const double r1 = warp_sum(a1[c]), r2 = warp_sum(a2[c]);
+      if (lane == 0) {
+        partial[(size_t)blockIdx.x * pld + i] = r1;
+        partial[(size_t)blockIdx.x * pld + k + i] = r2;
+      }
+    }
+  }
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) last = (atomicAdd(counters + s, 1u) == (unsigned)S.gps - 1u);
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  for (int i = warp; i < 2 * k; i += 2 * NW) {
+    const int i2 = i + NW;
+    if (i2 < 2 * k) {
+      double a, a2v;
+      partial_sum2(partial, (size_t)s * S.gps, pld, S.gps, i, i2, lane, a, a2v);
+      if (lane == 0) {
+        out[(size_t)s * ldo + i] = a;
+        out[(size_t)s * ldo + i2] = a2v;
+      }
+    } else {
+      const double a = partial_sum(partial, (size_t)s * S.gps, pld, S.gps, i, lane);
+      if (lane == 0) out[(size_t)s * ldo + i] = a;
+    }
+  }
+  if (tid == 0) counters[s] = 0u;
+  __syncthreads();
+  epi(s);
+}
+
 template <int KW, int MINB, int UN, class Epi = NoEpi>
 static __global__ void __launch_bounds__(256, MINB) k_dcgs_dots_direct(
     Seg S, int k, const double* __restrict__ V, int64_t ldv, const double* __restrict__ z, double* partial,
@@ -1003,6 +1111,35 @@ inline int launch_dcgs_dots_epi(const vec::Seg& S, int k, const double* V, int64
   const bool direct = direct_env && S.nseg == 1;
   // register-direct reduction pass: every owned column's loads of a tile issued
   // before its FMAs (UN = 0), columns per warp KW by k (fewer registers for small k)
+  // CPM_DOTS_TMA=1: the TMA-staged variant (measured slower: 42.3 against 33.1 ms per
+  // 204 passes of a config-1 solve; the per-tile block barrier of the ring) — A/B only
+  static const bool tma = [] {
+    const char* v = getenv("CPM_DOTS_TMA");
+    return v && *v == '1';
+  }();
+  if (direct && tma && k <= 8 * 17) {
+    // ring depth: up to 8 stages within ~100 KB (two blocks per SM); one stage (no
+    // overlap inside the block) when a stage alone exceeds that (k > 96)
+    const size_t stage = (size_t)(k + 1) * 128 * sizeof(double);
+    const int ns = (int)std::max<size_t>(1, std::min<size_t>(8, (100 * 1024) / stage));
+    static bool attr[4] = {false, false, false, false};  // per kernel variant
+    auto run = [&](auto kern, int v) -> int {
+      if (!attr[v]) {
+        CPM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        attr[v] = true;
+      }
+      CPM_CUDA(launch_pdl(kern, dim3(grid), dim3(256), ns * stage, st, S, k, V, ldv, z, partial, pld, out, ldo,
+                          counters, skip, ns, epi));
+      return CPM_OK;
+    };
+    if (k <= 8 * 2) CPM_TRY(run(vec::k_dcgs_dots_tma<2, Epi>, 0));
+    else if (k <= 8 * 4) CPM_TRY(run(vec::k_dcgs_dots_tma<4, Epi>, 1));
+    else if (k <= 8 * 8) CPM_TRY(run(vec::k_dcgs_dots_tma<8, Epi>, 2));
+    else CPM_TRY(run(vec::k_dcgs_dots_tma<17, Epi>, 3));
+    count_launch();
+    CPM_CUDA(cudaGetLastError());
+    return CPM_OK;
+  }
   static const int tt = [] {  // CPM_DOTS_TT=1: one tile per iteration also for k <= 32 (A/B)
     const char* v = getenv("CPM_DOTS_TT");
     return v ? atoi(v) : 2;
