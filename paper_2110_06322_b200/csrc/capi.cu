@@ -234,20 +234,32 @@ int cpm_apply_async(const cpm_band* b, double c, const double* u, double* y, voi
   if (!is_pinned_host(u) || !is_pinned_host(y)) return cpm_apply(b, c, u, y, stream);
   cudaStream_t s = (cudaStream_t)stream;
   cpm_band* mb = const_cast<cpm_band*>(b);
-  if (!mb->as) {
+  if (!mb->as) {  // staging slots, streams, events: all or nothing
     auto* a = new cpm_band::AsyncStage();
-    mb->as = a;
-    for (int q = 0; q < 2; ++q) {
-      CPM_CUDA(cudaMalloc(&a->u[q], sizeof(double) * std::max<int64_t>(b->nA, 1)));
-      CPM_CUDA(cudaMalloc(&a->y[q], sizeof(double) * std::max<int64_t>(b->nA, 1)));
-      CPM_CUDA(cudaEventCreateWithFlags(&a->ein[q], cudaEventDisableTiming));
-      CPM_CUDA(cudaEventCreateWithFlags(&a->ek[q], cudaEventDisableTiming));
-      CPM_CUDA(cudaEventCreateWithFlags(&a->eout[q], cudaEventDisableTiming));
-      CPM_CUDA(cudaEventRecord(a->ek[q], s));
-      CPM_CUDA(cudaEventRecord(a->eout[q], s));
+    bool ok = true;
+    const size_t bytes = sizeof(double) * std::max<int64_t>(b->nA, 1);
+    for (int q = 0; q < 2 && ok; ++q) {
+      ok = cudaMalloc(&a->u[q], bytes) == cudaSuccess && cudaMalloc(&a->y[q], bytes) == cudaSuccess &&
+           cudaEventCreateWithFlags(&a->ein[q], cudaEventDisableTiming) == cudaSuccess &&
+           cudaEventCreateWithFlags(&a->ek[q], cudaEventDisableTiming) == cudaSuccess &&
+           cudaEventCreateWithFlags(&a->eout[q], cudaEventDisableTiming) == cudaSuccess &&
+           cudaEventRecord(a->ek[q], s) == cudaSuccess && cudaEventRecord(a->eout[q], s) == cudaSuccess;
     }
-    CPM_CUDA(cudaStreamCreateWithFlags(&a->in, cudaStreamNonBlocking));
-    CPM_CUDA(cudaStreamCreateWithFlags(&a->out, cudaStreamNonBlocking));
+    ok = ok && cudaStreamCreateWithFlags(&a->in, cudaStreamNonBlocking) == cudaSuccess &&
+         cudaStreamCreateWithFlags(&a->out, cudaStreamNonBlocking) == cudaSuccess;
+    if (!ok) {
+      cudaGetLastError();
+      for (int q = 0; q < 2; ++q) {
+        if (a->u[q]) cudaFree(a->u[q]);
+        if (a->y[q]) cudaFree(a->y[q]);
+        for (cudaEvent_t e : {a->ein[q], a->ek[q], a->eout[q]})
+          if (e) cudaEventDestroy(e);
+      }
+      if (a->in) cudaStreamDestroy(a->in);
+      delete a;
+      return fail(CPM_ERR_NOMEM, "cpm_apply_async: staging allocation failed");
+    }
+    mb->as = a;
   }
   cpm_band::AsyncStage* a = mb->as;
   const int q = (int)(a->calls++ & 1u);

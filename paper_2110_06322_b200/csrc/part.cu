@@ -491,10 +491,10 @@ int part_apply(const cpm_part* P, const cpm_comm* comm, double c, const double* 
     return apply_device_split(L, c, x, P->hbuf, y, scale, 0, s, skip);
   }
   cpm_part* mp = const_cast<cpm_part*>(P);
-  if (!mp->xs) {
-    CPM_CUDA(cudaStreamCreateWithFlags(&mp->xs, cudaStreamNonBlocking));
-    CPM_CUDA(cudaEventCreateWithFlags(&mp->xev[0], cudaEventDisableTiming));
-    CPM_CUDA(cudaEventCreateWithFlags(&mp->xev[1], cudaEventDisableTiming));
+  if (!mp->xs || !mp->xev[0] || !mp->xev[1]) {  // (a failed earlier attempt leaves nulls)
+    if (!mp->xs) CPM_CUDA(cudaStreamCreateWithFlags(&mp->xs, cudaStreamNonBlocking));
+    if (!mp->xev[0]) CPM_CUDA(cudaEventCreateWithFlags(&mp->xev[0], cudaEventDisableTiming));
+    if (!mp->xev[1]) CPM_CUDA(cudaEventCreateWithFlags(&mp->xev[1], cudaEventDisableTiming));
   }
   CPM_CUDA(cudaEventRecord(mp->xev[0], s));  // x produced; the previous apply read hbuf
   CPM_CUDA(cudaStreamWaitEvent(mp->xs, mp->xev[0], 0));
