@@ -10,6 +10,8 @@
 
 #include "../../include/cpm.h"
 
+struct cpm_band;
+
 namespace cpm {
 
 constexpr int kBrick = 8;                 // brick edge (lattice cells)
@@ -67,6 +69,43 @@ inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
+// L2 persistence window of a launch (the E u bricks between extend and laplace,
+// apply.cu): {base, bytes}; bytes == 0: none.
+struct L2Window {
+  void* base = nullptr;
+  size_t bytes = 0;
+  float hit = 1.0f;
+};
+L2Window vb_window(const cpm_band* b);  // apply.cu
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl_l2(const L2Window& w, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                                 cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[2];
+  int na = 0;
+  if (pdl_enabled()) {
+    at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  if (w.bytes) {
+    at[na].id = cudaLaunchAttributeAccessPolicyWindow;
+    at[na].val.accessPolicyWindow.base_ptr = w.base;
+    at[na].val.accessPolicyWindow.num_bytes = w.bytes;
+    at[na].val.accessPolicyWindow.hitRatio = w.hit;
+    at[na].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    at[na].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    ++na;
+  }
+  cfg.attrs = at;
+  cfg.numAttrs = na;
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
