@@ -653,7 +653,7 @@ def run_partitioned(args):
                 torch.cuda.synchronize()
                 (sec,) = max_over_ranks([a.elapsed_time(b) / 1e3])
                 rr = sum_over_ranks([cst.resid_true ** 2])
-                c2 = {"workload": "BASELINE configs[2] partitioned over the ranks (Morton slabs, NCCL halo "
+                c2 = {"workload": f"BASELINE configs[2] partitioned over the ranks (Morton slabs, {transport} halo "
                                   "exchange + allreduce, distributed RAS: 8 subdomains, overlap 4h, "
                                   f"{args.c2_kinner} inner GMRES steps), RAS-FGMRES(50), rtol 1e-10",
                       "ranks": ws, "n_active": tb.n, "solve_s": sec, "iterations": cst.iterations,
@@ -710,7 +710,8 @@ def run_partitioned(args):
                        "rank0_interior_tiles": pinfo.n_interior_tiles,
                        "l2": "inputs larger than L2 at N <= 4; the timed applies include the halo exchange"},
             "solve": {"seconds_median": solve_ms / 1e3, "iterations": st.iterations, "converged": st.converged,
-                      "resid_true_rel": st.resid_true / st.bnorm, "kind": "partitioned GMRES(50) (NCCL allreduce)"},
+                      "resid_true_rel": st.resid_true / st.bnorm,
+                      "kind": f"partitioned GMRES(50) ({'host-transport' if host else 'NCCL'} allreduce)"},
             "setup_s": setup_s,
             "roofline": {"kernel": "apply = halo exchange + k_extend_nt + k_laplace on each rank's sub-band",
                          "bound": "hbm", "achieved": achieved_per_gpu, "peak": peak, "unit": "GB/s",
