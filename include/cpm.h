@@ -112,15 +112,23 @@ int cpm_band_get_info(const cpm_band* band, cpm_band_info* info);
  * a HOST int32 array of 3*n entries. */
 int cpm_band_active_coords(const cpm_band* band, int32_t* ijk_host);
 int cpm_band_ghost_coords(const cpm_band* band, int32_t* ijk_host);
-/* Diagnostics of the extend's node order (build.cu k_warp_order; DESIGN.md
- * §Kernels): per tile 6 int32 into tiles_host[6*n_tiles] = e0, e1 (eval-node
- * range, padded index space), np | nd << 16 (np equal-base pairs at e0 + 2p,
+/* Diagnostics of the extend's node order (build.cu k_item_order / k_warp_order;
+ * DESIGN.md §Kernels): per tile 6 int32 into tiles_host[6*n_tiles] = e0, e1
+ * (eval-node range, padded index space), the order word — item order (the
+ * default): 1 << 30 | number of rounds (cpm_band_item_rounds); pair order
+ * (CPM_ITEMS=0 at build): np | nd << 16 (np equal-base pairs at e0 + 2p,
  * e0 + 2p + 1; then nd unpaired nodes gathered by lane pairs, the rest one per lane),
  * row stride and plane stride of the tile's stencil box, box cells; and, if
  * eoff_host is not null, the packed stencil-base offsets (low 16 bits: offset
  * in the box, high 16: brick cell) of the padded eval index space [0, e1 of the
  * last tile) into eoff_host.  Read-only; CPM_ERR_ARG on null band/tiles_host. */
 int cpm_band_eval_order(const cpm_band* band, int32_t* tiles_host, uint32_t* eoff_host);
+/* The item rounds of an item-order band (build.cu k_item_order): 32 uint64 per
+ * tile into rounds_host[32*n_tiles] (unused words 0).  Word bits 0-31: lane l's
+ * item holds two nodes; 32-47: the round's first node relative to the tile's e0;
+ * 48-53: lanes in use.  Lane l's item starts at that node + l + popcount(bits
+ * below l).  Read-only; CPM_ERR_ARG on a null argument or a pair-order band. */
+int cpm_band_item_rounds(const cpm_band* band, uint64_t* rounds_host);
 void cpm_band_free(cpm_band* band);
 
 /* ---------------------------------------------------------------- operator apply

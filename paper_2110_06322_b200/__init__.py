@@ -13,6 +13,7 @@ from .cpm import (  # noqa: F401
     cpm_apply_sync,
     cpm_band_active_coords,
     cpm_band_eval_order,
+    cpm_band_item_rounds,
     cpm_band_ghost_coords,
     cpm_build_band,
     cpm_comm_init,

@@ -90,6 +90,7 @@ _SIGS = {
     "cpm_band_active_coords": (ctypes.c_int, [_vp, _vp]),
     "cpm_band_ghost_coords": (ctypes.c_int, [_vp, _vp]),
     "cpm_band_eval_order": (ctypes.c_int, [_vp, _vp, _vp]),
+    "cpm_band_item_rounds": (ctypes.c_int, [_vp, _vp]),
     "cpm_band_free": (None, [_vp]),
     "cpm_apply": (ctypes.c_int, [_vp, ctypes.c_double, _vp, _vp, _vp]),
     "cpm_apply_async": (ctypes.c_int, [_vp, ctypes.c_double, _vp, _vp, _vp]),
@@ -277,6 +278,13 @@ def cpm_band_eval_order(band: Band):
     eoff = np.empty(ne, dtype=np.uint32)
     _check(lib.cpm_band_eval_order(band.handle, tiles.ctypes.data, eoff.ctypes.data), "cpm_band_eval_order")
     return tiles, eoff
+
+
+def cpm_band_item_rounds(band: Band):
+    """rounds[n_tiles, 32] (uint64) — the item rounds of an item-order band (include/cpm.h)."""
+    out = np.zeros((band.info.n_tiles, 32), dtype=np.uint64)
+    _check(load_library().cpm_band_item_rounds(band.handle, out.ctypes.data), "cpm_band_item_rounds")
+    return out
 
 
 def cpm_apply(band: Band, c: float, u, y, stream=None):

@@ -21,8 +21,11 @@
 // No tensor cores: this is a gather, not a dense contraction.  The extend is
 // bound by its per-tile load chain overlapped with FP64 issue and shared-memory
 // gathers, the laplace by load latency; DESIGN.md §Kernels has the measurements.
+#include <cuda.h>
+
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 
 #include "internal.cuh"
 
@@ -243,6 +246,161 @@ __global__ void __launch_bounds__(kNtThreads, 8)
   }
 }
 
+// ------------------------------------------------------------------ item extend
+// The default extend (bands in item order, build.cu k_item_order): as k_extend_nt,
+// but a lane evaluates an ITEM of one or two equal-base nodes, so each of its 64
+// shared-memory gathers feeds two contractions; warp w takes the tile's rounds
+// w, w + 4, ...  Per node the arithmetic is contract_node's, operation for
+// operation, so E u is bit-identical to the pair order's.
+struct ItemLane {
+  int i;       // first node (absolute eval index), -1 = idle lane
+  bool two;    // a second node at i + 1
+};
+__device__ __forceinline__ ItemLane item_of(uint64_t w, int e0, int lane) {
+  ItemLane it;
+  const uint32_t flags = (uint32_t)w;
+  const int base = (int)((w >> 32) & 0xffffu), nv = (int)((w >> 48) & 0x3fu);
+  it.i = lane < nv ? e0 + base + lane + __popc(flags & ((1u << lane) - 1u)) : -1;
+  it.two = (flags >> lane) & 1u;
+  return it;
+}
+
+__device__ __forceinline__ void contract_item(const double (&ta)[3], const double (&tb)[3], uint32_t eoa,
+                                              uint32_t eob, bool two, const double* __restrict__ box, int sx,
+                                              int sxy, double* __restrict__ out, uint64_t pol) {
+  double ax[4], ay[4], az[4], bx[4], by[4], bz[4];
+  lagrange4(ta[0], ax);
+  lagrange4(ta[1], ay);
+  lagrange4(ta[2], az);
+  lagrange4(tb[0], bx);
+  lagrange4(tb[1], by);
+  lagrange4(tb[2], bz);
+  const double* p = box + (eoa & 0xffffu);
+  double acca = 0.0, accb = 0.0;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    double ya = 0.0, yb = 0.0;
+#pragma unroll
+    for (int bb = 0; bb < 4; ++bb) {
+      const double* row = p + bb * sx + c * sxy;
+      const double r0 = row[0], r1 = row[1], r2 = row[2], r3 = row[3];
+      ya += ay[bb] * ((ax[0] * r0 + ax[1] * r1) + (ax[2] * r2 + ax[3] * r3));
+      yb += by[bb] * ((bx[0] * r0 + bx[1] * r1) + (bx[2] * r2 + bx[3] * r3));
+    }
+    acca += az[c] * ya;
+    accb += bz[c] * yb;
+  }
+  st_hint(out + (eoa >> 16), acca, pol);
+  if (two) st_hint(out + (eob >> 16), accb, pol);
+}
+
+template <bool ZERO, int MINB>
+__global__ void __launch_bounds__(kNtThreads, MINB)
+    k_extend_it(const TileHdr* __restrict__ tiles, int boxCells, int descCap,
+                const uint64_t* __restrict__ runs, const double* __restrict__ u,
+                const double* __restrict__ uh, uint32_t split, const double* __restrict__ tx,
+                const double* __restrict__ ty, const double* __restrict__ tz,
+                const uint32_t* __restrict__ eoff, const uint64_t* __restrict__ rnd,
+                double* __restrict__ vb, const int* __restrict__ skip, int pfd, int tbase, int tend) {
+  extern __shared__ double smn[];
+  double* box = smn;
+  uint64_t* desc = (uint64_t*)(box + boxCells);
+  const int t = tbase + (int)blockIdx.x, tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const TileHdr* T = tiles + t;
+  const int e0 = T->e0, r0 = T->r0, r1 = T->r1;
+  const int q0 = T->np, nq = T->pad2;
+  const int sx = T->pad[0], sxy = T->pad[1];
+  const uint64_t pfirst = policy_evict_first(), plast = policy_evict_last();
+  // this warp's first round: its items' offsets are requested before the box is staged
+  double ta[3] = {0.0, 0.0, 0.0}, tb[3] = {0.0, 0.0, 0.0};
+  uint32_t eoa = 0, eob = 0;
+  ItemLane it{-1, false};
+  bool single = false;
+  if (warp < nq) {
+    const uint64_t w = __ldg(rnd + q0 + warp);
+    single = (uint32_t)w == 0u;
+    it = item_of(w, e0, lane);
+    if (it.i >= 0) {
+      const int j = it.two ? it.i + 1 : it.i;
+      ta[0] = ld_hint(tx + it.i, pfirst);
+      ta[1] = ld_hint(ty + it.i, pfirst);
+      ta[2] = ld_hint(tz + it.i, pfirst);
+      eoa = ld_hint(eoff + it.i, pfirst);
+      tb[0] = ld_hint(tx + j, pfirst);
+      tb[1] = ld_hint(ty + j, pfirst);
+      tb[2] = ld_hint(tz + j, pfirst);
+      eob = ld_hint(eoff + j, pfirst);
+    }
+  }
+  if (ZERO) {
+    const int nbox = sxy * T->sz;
+    for (int c = tid; c < nbox; c += kNtThreads) box[c] = 0.0;
+  }
+  const int g = tid >> 3, l = tid & 7;
+  int nr = min(descCap, r1 - r0);
+  for (int r = tid; r < nr; r += kNtThreads) cp_async8_hint(desc + r, runs + r0 + r, pfirst);
+  cp_commit();
+  pdl_wait();
+  if (skip && *skip) {
+    cp_wait<0>();
+    return;
+  }
+  for (int c0 = r0; c0 < r1; c0 += nr, nr = min(descCap, r1 - c0)) {
+    if (c0 > r0) {
+      __syncthreads();
+      for (int r = tid; r < nr; r += kNtThreads) cp_async8_hint(desc + r, runs + c0 + r, pfirst);
+      cp_commit();
+    }
+    cp_wait<0>();
+    __syncthreads();
+    for (int r = g; r < nr; r += kNtThreads / 8) {
+      const uint64_t d = desc[r];
+      const uint32_t src = (uint32_t)d, dst = (uint32_t)(d >> 32) & 0xffffu,
+                     len = (uint32_t)(d >> 48) & 0xffu;
+      if (l < len) {
+        const double* gsrc = src >= split ? uh + (src - split) : u + src;
+        cp_async8_hint(box + dst + l, gsrc + l, plast);
+      }
+    }
+    cp_commit();
+  }
+  if (tid == kNtThreads - 32 && t + pfd < tend) {
+    const TileHdr* F = tiles + t + pfd;
+    const int f0 = F->e0, f1 = F->e1, fq0 = F->r0, fq1 = F->r1;
+    prefetch_l2_bytes(runs + fq0, (size_t)(fq1 - fq0) * 8);
+    prefetch_l2_bytes(tx + f0, (size_t)(f1 - f0) * 8);
+    prefetch_l2_bytes(ty + f0, (size_t)(f1 - f0) * 8);
+    prefetch_l2_bytes(tz + f0, (size_t)(f1 - f0) * 8);
+    prefetch_l2_bytes(eoff + f0, (size_t)(f1 - f0) * 4);
+    prefetch_l2_bytes(rnd + F->np, (size_t)F->pad2 * 8);
+    if (t + 2 * pfd < tend) prefetch_l2_bytes(tiles + t + 2 * pfd, sizeof(TileHdr));
+  }
+  cp_wait<0>();
+  __syncthreads();
+  double* out = vb + (size_t)t * kBrickCells;
+  // rounds without a two-node item (warp-uniform flags == 0) run the single contraction
+  if (it.i >= 0) {
+    if (single) contract_node(ta, eoa, box, sx, sxy, out, true, plast);
+    else contract_item(ta, tb, eoa, eob, it.two, box, sx, sxy, out, plast);
+  }
+  for (int q = warp + kNtThreads / 32; q < nq; q += kNtThreads / 32) {
+    const uint64_t w = __ldg(rnd + q0 + q);
+    it = item_of(w, e0, lane);
+    if (it.i >= 0) {
+      const double a3[3] = {ld_hint(tx + it.i, pfirst), ld_hint(ty + it.i, pfirst), ld_hint(tz + it.i, pfirst)};
+      const uint32_t ea = ld_hint(eoff + it.i, pfirst);
+      if ((uint32_t)w == 0u) {
+        contract_node(a3, ea, box, sx, sxy, out, true, plast);
+      } else {
+        const int j = it.two ? it.i + 1 : it.i;
+        const double b3[3] = {ld_hint(tx + j, pfirst), ld_hint(ty + j, pfirst), ld_hint(tz + j, pfirst)};
+        contract_item(a3, b3, ea, ld_hint(eoff + j, pfirst), it.two, box, sx, sxy, out, plast);
+      }
+    }
+  }
+}
+
 // Dense halo brick: cell (x, y, z), x, y, z in -1..8, at (x+1) + 10 (y+1) + 100 (z+1).
 __device__ __forceinline__ int hidx(int x, int y, int z) { return (x + 1) + 10 * (y + 1) + 100 * (z + 1); }
 
@@ -333,6 +491,111 @@ __global__ void __launch_bounds__(kLapThreads) k_laplace(const TileHdr* __restri
   }
 }
 
+
+// ------------------------------------------------------------------ TMA laplace
+// One CTA (128 threads) per tile; every E u load is a TMA copy issued by one
+// thread after pdl_wait(): the own brick (4 KB bulk copy of vb slot t), the two
+// z face layers of the z neighbours (512 B bulk copies), the y face layers (tensor
+// copy, box 8 x 1 x 8 of the neighbour's brick) and the x face layers (tensor copy,
+// box 2 x 8 x 8: 16-byte inner extent, the wanted layer and one more).  The copies
+// land on one mbarrier; no per-element global loads, no emask test.  Then the
+// 7-point combination in the same operation order as k_laplace (bit-identical).
+__device__ __forceinline__ unsigned sm32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void tma_bulk(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(sm32(dst)),
+      "l"(src), "r"(bytes), "r"(sm32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_4d(void* dst, const CUtensorMap* tm, int x, int y, int z, int t, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
+      "[%6];\n" ::"r"(sm32(dst)),
+      "l"(tm), "r"(x), "r"(y), "r"(z), "r"(t), "r"(sm32(bar))
+      : "memory");
+}
+
+__global__ void __launch_bounds__(128, 16) k_laplace_tma(const TileHdr* __restrict__ tiles, const double* __restrict__ u,
+                                                     const uint16_t* __restrict__ acell,
+                                                     const double* __restrict__ vb, double* __restrict__ y,
+                                                     double diag, double ih2, const double* __restrict__ scale,
+                                                     int lds, const int* __restrict__ skip, int pfd,
+                                                     const __grid_constant__ CUtensorMap tmX,
+                                                     const __grid_constant__ CUtensorMap tmY) {
+  __shared__ __align__(128) double own[512];
+  __shared__ __align__(128) double fx[2][128];  // [+x, -x] box 2 x 8 x 8: x + 2 y + 16 z
+  __shared__ __align__(128) double fy[2][64];   // [+y, -y] box 8 x 1 x 8: x + 8 z
+  __shared__ __align__(128) double fz[2][64];   // [+z, -z] layer: x + 8 y
+  __shared__ uint64_t bar;
+  const int t = (int)gridDim.x - 1 - (int)blockIdx.x, tid = threadIdx.x;
+  const TileHdr* T = tiles + t;
+  const int a0 = T->a0, a1 = T->a1;
+  if (a0 == a1) return;
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(sm32(&bar)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (tid == 32 && t - pfd >= 0) {  // a later CTA's tile into L2
+    const TileHdr* F = tiles + t - pfd;
+    const int f0 = F->a0, f1 = F->a1;
+    prefetch_l2_bytes(acell + f0, (size_t)(f1 - f0) * 2);
+    prefetch_l2_bytes(u + f0, (size_t)(f1 - f0) * 8);
+    prefetch_l2_bytes(vb + (size_t)(t - pfd) * kBrickCells, kBrickCells * 8);
+  }
+  int ac[4];
+  double au[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int a = a0 + tid + k * 128;
+    if (a < a1) ac[k] = __ldg(acell + a);
+  }
+  __syncthreads();  // mbarrier initialised
+  pdl_wait();       // the extend (E u) and the producer of u have completed
+  if (skip && *skip) return;
+  if (tid == 0) {
+    int nb[6];
+    unsigned bytes = kBrickCells * 8;
+#pragma unroll
+    for (int f = 0; f < 6; ++f) {
+      nb[f] = T->nbr[f];
+      if (nb[f] >= 0) bytes += f < 2 ? 1024u : 512u;
+    }
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(sm32(&bar)), "r"(bytes)
+                 : "memory");
+    tma_bulk(own, vb + (size_t)t * kBrickCells, kBrickCells * 8, &bar);
+    if (nb[0] >= 0) tma_4d(fx[0], &tmX, 0, 0, 0, nb[0], &bar);  // +x neighbour: its x = 0 layer
+    if (nb[1] >= 0) tma_4d(fx[1], &tmX, 6, 0, 0, nb[1], &bar);  // -x neighbour: x = 7 (box x = 6, 7)
+    if (nb[2] >= 0) tma_4d(fy[0], &tmY, 0, 0, 0, nb[2], &bar);
+    if (nb[3] >= 0) tma_4d(fy[1], &tmY, 0, 7, 0, nb[3], &bar);
+    if (nb[4] >= 0) tma_bulk(fz[0], vb + (size_t)nb[4] * kBrickCells, 512, &bar);
+    if (nb[5] >= 0) tma_bulk(fz[1], vb + (size_t)nb[5] * kBrickCells + 448, 512, &bar);
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int a = a0 + tid + k * 128;
+    if (a < a1) au[k] = __ldg(u + a);
+  }
+  const double s = scale ? __ldg(scale + (size_t)T->pad[2] * lds) : 1.0;
+  asm volatile(
+      "{\n .reg .pred p;\n WAITL_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n"
+      " @!p bra WAITL_%=;\n}\n" ::"r"(sm32(&bar))
+      : "memory");
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int a = a0 + tid + k * 128;
+    if (a < a1) {
+      const int c = ac[k], x = c & 7, yy = (c >> 3) & 7, z = c >> 6;
+      const double xp = x < 7 ? own[c + 1] : fx[0][2 * yy + 16 * z];
+      const double xm = x > 0 ? own[c - 1] : fx[1][1 + 2 * yy + 16 * z];
+      const double yp = yy < 7 ? own[c + 8] : fy[0][x + 8 * z];
+      const double ym = yy > 0 ? own[c - 8] : fy[1][x + 8 * z];
+      const double zp = z < 7 ? own[c + 64] : fz[0][x + 8 * yy];
+      const double zm = z > 0 ? own[c - 64] : fz[1][x + 8 * yy];
+      const double sum = xp + xm + yp + ym + zp + zm;
+      y[a] = s * (diag * au[k] - ih2 * sum);
+    }
+  }
+}
 
 // ------------------------------------------------------------------ fused apply (experiment)
 // One CTA (128 threads) per tile, no vb: stage the FUSED box (build.cu build_fused:
@@ -489,7 +752,10 @@ int extend_tiles(const cpm_band* b, const double* u, const double* uh, cudaStrea
   if (t1 <= t0) return CPM_OK;
   const int pfd = prefetch_distance();
   const int descCap = 512;
-  const size_t smem = (size_t)b->maxBox * 8 + (size_t)descCap * 8;
+  // CPM_EXT_SMEM_PAD (bytes, experiment): extra dynamic shared memory per CTA, to
+  // measure the extend's sensitivity to resident CTAs per SM
+  static const size_t smpad = getenv("CPM_EXT_SMEM_PAD") ? (size_t)atol(getenv("CPM_EXT_SMEM_PAD")) : 0;
+  const size_t smem = (size_t)b->maxBox * 8 + (size_t)descCap * 8 + smpad;
   ProfScope ps(K_EXTEND, s);
 #define CPM_EXTNT(Z)                                                                         \
   do {                                                                                       \
@@ -504,10 +770,71 @@ int extend_tiles(const cpm_band* b, const double* u, const double* uh, cudaStrea
                         (uint32_t)b->srcSplit, (const double*)b->tx, (const double*)b->ty,      \
                         (const double*)b->tz, (const uint32_t*)b->eoff, b->vb, skip, pfd, t0, t1)); \
   } while (0)
-  if (b->zeroFill) CPM_EXTNT(true); else CPM_EXTNT(false);
+#define CPM_EXTIT(Z, MB)                                                                       \
+  do {                                                                                       \
+    static bool attr = false;                                                                \
+    if (!attr) {                                                                             \
+      CPM_CUDA(cudaFuncSetAttribute(k_extend_it<Z, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                    227 * 1024));                                            \
+      attr = true;                                                                           \
+    }                                                                                        \
+    CPM_CUDA(launch_pdl_l2(vb_window(b), k_extend_it<Z, MB>, dim3((unsigned)(t1 - t0)), dim3(kNtThreads), smem, s, \
+                        b->tiles, (int)b->maxBox, descCap, (const uint64_t*)b->runs, u, uh,     \
+                        (uint32_t)b->srcSplit, (const double*)b->tx, (const double*)b->ty,      \
+                        (const double*)b->tz, (const uint32_t*)b->eoff, (const uint64_t*)b->rnd, \
+                        b->vb, skip, pfd, t0, t1));                                              \
+  } while (0)
+  static const int minb = getenv("CPM_IT_MINB") ? atoi(getenv("CPM_IT_MINB")) : 6;
+  if (b->itemOrder) {
+    if (minb == 8) {
+      if (b->zeroFill) CPM_EXTIT(true, 8); else CPM_EXTIT(false, 8);
+    } else if (minb == 7) {
+      if (b->zeroFill) CPM_EXTIT(true, 7); else CPM_EXTIT(false, 7);
+    } else {
+      if (b->zeroFill) CPM_EXTIT(true, 6); else CPM_EXTIT(false, 6);
+    }
+  } else {
+    if (b->zeroFill) CPM_EXTNT(true); else CPM_EXTNT(false);
+  }
 #undef CPM_EXTNT
+#undef CPM_EXTIT
   count_launch();
   CPM_CUDA(cudaGetLastError());
+  return CPM_OK;
+}
+
+// Tensor maps over vb viewed as [nT][8][8][8] doubles (x fastest) for the TMA
+// laplace's face copies: box 2 x 8 x 8 (x faces) and 8 x 1 x 8 (y faces).  Built
+// once per band (vb and nT are fixed), cached in the band.
+static int laplace_tmaps(const cpm_band* b) {
+  if (b->tmReady) return CPM_OK;
+  using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static EncodeFn enc = []() -> EncodeFn {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return nullptr;
+    return (EncodeFn)fn;
+  }();
+  if (!enc) return fail(CPM_ERR_CUDA, "laplace: cuTensorMapEncodeTiled unavailable");
+  const cuuint64_t dims[4] = {8, 8, 8, (cuuint64_t)b->nT};
+  const cuuint64_t strides[3] = {64, 512, 4096};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  const cuuint32_t boxX[4] = {2, 8, 8, 1}, boxY[4] = {8, 1, 8, 1};
+  CUtensorMap mx, my;
+  for (int q = 0; q < 2; ++q) {
+    const CUresult r = enc(q ? &my : &mx, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, b->vb, dims, strides,
+                           q ? boxY : boxX, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(CPM_ERR_CUDA, "laplace: tensor map encoding failed");
+  }
+  cpm_band* mb = const_cast<cpm_band*>(b);
+  std::memcpy(mb->tmX, &mx, sizeof(CUtensorMap));
+  std::memcpy(mb->tmY, &my, sizeof(CUtensorMap));
+  mb->tmReady = true;
   return CPM_OK;
 }
 
@@ -518,6 +845,19 @@ int laplace_tiles(const cpm_band* b, double c, const double* u, double* y, const
   ProfScope ps(K_LAPLACE, s);
   // 128 threads per tile: 16 resident tiles per SM keep enough loads in flight
   static const int pfd2 = getenv("CPM_LAP_PFD") ? atoi(getenv("CPM_LAP_PFD")) : prefetch_distance();
+  static const bool tma = !(getenv("CPM_LAP_TMA") && *getenv("CPM_LAP_TMA") == '0');
+  if (tma) {
+    CPM_TRY(laplace_tmaps(b));
+    CUtensorMap mx, my;
+    std::memcpy(&mx, b->tmX, sizeof(CUtensorMap));
+    std::memcpy(&my, b->tmY, sizeof(CUtensorMap));
+    CPM_CUDA(launch_pdl_l2(vb_window(b), k_laplace_tma, dim3((unsigned)b->nT), dim3(128), 0, s, b->tiles, u,
+                           (const uint16_t*)b->acell, (const double*)b->vb, y, diag, ih2, scale, lds, skip, pfd2,
+                           mx, my));
+    count_launch();
+    CPM_CUDA(cudaGetLastError());
+    return CPM_OK;
+  }
   CPM_CUDA(launch_pdl_l2(vb_window(b), k_laplace<128>, dim3((unsigned)b->nT), dim3(128), 0, s, b->tiles, u,
                       (const uint16_t*)b->acell, (const double*)b->vb, y, diag, ih2, scale, lds,
                       skip, pfd2));

@@ -352,41 +352,18 @@ __global__ void __launch_bounds__(512) k_sort_tile(const TileHdr* tiles, double*
   }
 }
 
-// ------------------------------------------------------------------ B6c
-// Warp order: k_extend_nt gives the tile's nodes 32 at a time to the lanes of a
-// warp.  An 8-byte shared-memory load of a warp costs ONE wavefront when every
-// adjacent lane pair (2i, 2i+1) reads the same double and the 16 pair addresses
-// fall in distinct bank pairs, two otherwise (measured, tools/micro/shfl_vs_lds.cu).
-// All 64 gathers of a node are its stencil base + a lane-independent row
-// offset, so: nodes of equal base are paired, pairs are dealt 16 to a warp with
-// box offsets that are distinct mod 16 or equal (greedy from the base-sorted
-// order; when no compatible pair is left, any); the unpaired nodes follow, dealt
-// 16 per half-warp by the same rule.
-// One CTA per tile, thread 0 plans.
-__global__ void __launch_bounds__(512) k_warp_order(TileHdr* tiles, double* tx, double* ty,
-                                                    double* tz, uint32_t* eoff, int boxCap) {
-  __shared__ double sv[3][512];
-  __shared__ uint32_t so[512];
-  __shared__ uint16_t perm[512], pfirst[256], single[512];
-  __shared__ uint8_t pused[512];
-  __shared__ int npair, ndup;
-  __shared__ unsigned long long best;
-  const TileHdr T = tiles[blockIdx.x];
-  const int n = T.e1 - T.e0, t = threadIdx.x;
-  if (t < n) {
-    sv[0][t] = tx[T.e0 + t];
-    sv[1][t] = ty[T.e0 + t];
-    sv[2][t] = tz[T.e0 + t];
-    so[t] = eoff[T.e0 + t];
-  }
+// Box strides for bank spread (both node orders): the dealing needs, per warp,
+// items with distinct stencil-base offsets mod 16, so choose the padded strides
+// (row stride sx + a, plane stride (sx + a) sy + b, a, b < 16) that make the
+// residues of the tile's distinct bases most uniform (largest minimum count, then
+// the smallest box), among those no larger than the band's largest box.  Bases
+// are decoded from the current offsets; so[] (sorted by offset) is re-encoded.
+// Called by all threads of a 512-thread CTA.
+__device__ void balance_strides(const TileHdr& T, TileHdr* hdr, uint32_t* so, int n, int boxCap,
+                                unsigned long long& best) {
+  const int t = threadIdx.x;
   if (t == 0) best = ~0ull;
   __syncthreads();
-  // Box strides for bank spread: the dealing below needs, per warp, 16 items with
-  // distinct stencil-base offsets mod 16, so choose the padded strides (row stride
-  // sx + a, plane stride (sx + a) sy + b, a, b < 16) that make the residues of the
-  // tile's distinct bases most uniform (largest minimum count, then the smallest
-  // box), among those no larger than the band's largest box.  Bases are decoded
-  // from the current offsets.
   {
     const int px0 = T.pad[0], pxy0 = T.pad[1];
     const int a = t & 15, b = (t >> 4) & 15;
@@ -422,10 +399,41 @@ __global__ void __launch_bounds__(512) k_warp_order(TileHdr* tiles, double* tx, 
     }
     __syncthreads();
     if (t == 0) {
-      tiles[blockIdx.x].pad[0] = px;
-      tiles[blockIdx.x].pad[1] = pxy;
+      hdr->pad[0] = px;
+      hdr->pad[1] = pxy;
     }
   }
+  __syncthreads();
+}
+
+// ------------------------------------------------------------------ B6c
+// Warp order: k_extend_nt gives the tile's nodes 32 at a time to the lanes of a
+// warp.  An 8-byte shared-memory load of a warp costs ONE wavefront when every
+// adjacent lane pair (2i, 2i+1) reads the same double and the 16 pair addresses
+// fall in distinct bank pairs, two otherwise (measured, tools/micro/shfl_vs_lds.cu).
+// All 64 gathers of a node are its stencil base + a lane-independent row
+// offset, so: nodes of equal base are paired, pairs are dealt 16 to a warp with
+// box offsets that are distinct mod 16 or equal (greedy from the base-sorted
+// order; when no compatible pair is left, any); the unpaired nodes follow, dealt
+// 16 per half-warp by the same rule.
+// One CTA per tile, thread 0 plans.
+__global__ void __launch_bounds__(512) k_warp_order(TileHdr* tiles, double* tx, double* ty,
+                                                    double* tz, uint32_t* eoff, int boxCap) {
+  __shared__ double sv[3][512];
+  __shared__ uint32_t so[512];
+  __shared__ uint16_t perm[512], pfirst[256], single[512];
+  __shared__ uint8_t pused[512];
+  __shared__ int npair, ndup;
+  __shared__ unsigned long long best;
+  const TileHdr T = tiles[blockIdx.x];
+  const int n = T.e1 - T.e0, t = threadIdx.x;
+  if (t < n) {
+    sv[0][t] = tx[T.e0 + t];
+    sv[1][t] = ty[T.e0 + t];
+    sv[2][t] = tz[T.e0 + t];
+    so[t] = eoff[T.e0 + t];
+  }
+  balance_strides(T, tiles + blockIdx.x, so, n, boxCap, best);
   if (t == 0) {
     int np = 0, ns = 0;
     for (int i = 0; i < n;) {  // groups of equal base -> pairs + a singleton
@@ -531,6 +539,145 @@ __global__ void __launch_bounds__(512) k_warp_order(TileHdr* tiles, double* tx, 
   }
 }
 
+// ------------------------------------------------------------------ B6d
+// Item order (the default; k_extend_it in apply.cu): a lane evaluates an ITEM of
+// one or two eval nodes with the same stencil base, so each of its 64 shared-memory
+// gathers feeds two contractions.  A warp load costs one wavefront per 16 distinct
+// doubles in distinct bank pairs (tools/micro/shfl_vs_lds.cu), so
+//   * groups of >= 3 equal-base nodes become CHUNKS of 3-4 nodes on a lane pair
+//     (2 + 1..2 nodes, one address for both lanes), dealt 16 per warp round with
+//     distinct offsets mod 16: one wavefront per gather for up to 64 nodes;
+//   * the rest (groups of 1-2, a chunk's remainder of 1-2) are LONE items, one
+//     per lane, 16 per half-warp with distinct residues: two wavefronts; rounds
+//     of two-node items, then rounds of one-node items (flags 0: the kernel runs
+//     the single contraction there).
+// Per tile the rounds are words in rnd[T.np .. T.np + T.pad2): bits 0-31 = lane l's
+// item has two nodes, bits 32-47 = the round's first node (relative to e0), bits
+// 48-53 = lanes in use.  Lane l's item starts at that node + l + popc(bits below l).
+// One CTA per tile, thread 0 plans.
+constexpr int kMaxRounds = 32;  // per tile: <= 512/3/16 chunk rounds + 512/32 lone rounds
+__global__ void __launch_bounds__(512) k_item_order(TileHdr* tiles, double* tx, double* ty,
+                                                    double* tz, uint32_t* eoff, uint64_t* rnd,
+                                                    int boxCap, int* err) {
+  __shared__ double sv[3][512];
+  __shared__ uint32_t so[512];
+  __shared__ uint16_t perm[512], cstart[512], lstart[512];
+  __shared__ uint8_t ccnt[512], lcnt[512], used[512];
+  __shared__ unsigned long long best;
+  const TileHdr T = tiles[blockIdx.x];
+  const int n = T.e1 - T.e0, t = threadIdx.x;
+  if (t < n) {
+    sv[0][t] = tx[T.e0 + t];
+    sv[1][t] = ty[T.e0 + t];
+    sv[2][t] = tz[T.e0 + t];
+    so[t] = eoff[T.e0 + t];
+  }
+  balance_strides(T, tiles + blockIdx.x, so, n, boxCap, best);
+  if (t == 0) {
+    uint64_t* R = rnd + (size_t)blockIdx.x * kMaxRounds;
+    int nc = 0, nl = 0;
+    for (int i = 0; i < n;) {  // equal-base groups -> chunks of 3-4, lone items of 1-2
+      int j = i + 1;
+      while (j < n && (so[j] & 0xffffu) == (so[i] & 0xffffu)) ++j;
+      int q = i;
+      while (j - q >= 3) {
+        const int c = min(4, j - q);
+        cstart[nc] = (uint16_t)q;
+        ccnt[nc++] = (uint8_t)c;
+        q += c;
+      }
+      if (q < j) {
+        lstart[nl] = (uint16_t)q;
+        lcnt[nl++] = (uint8_t)(j - q);
+      }
+      i = j;
+    }
+    int out = 0, nr = 0;
+    // chunk rounds: 16 chunks with distinct residues (compatible first, then any)
+    for (int q = 0; q < nc; ++q) used[q] = 0;
+    int left = nc, first = 0;
+    while (left > 0) {
+      uint32_t res = 0, flags = 0;
+      int taken = 0;
+      const int base = out;
+      for (int pass = 0; pass < 2 && taken < 16 && left > 0; ++pass)
+        for (int q = first; q < nc && taken < 16; ++q) {
+          if (used[q]) continue;
+          const uint32_t r = so[cstart[q]] & 15u;
+          if (pass == 0 && ((res >> r) & 1u)) continue;
+          res |= 1u << r;
+          used[q] = 1;
+          --left;
+          const int s0 = cstart[q], c = ccnt[q];
+          perm[out++] = (uint16_t)s0;  // lane 2k: two nodes
+          perm[out++] = (uint16_t)(s0 + 1);
+          flags |= 1u << (2 * taken);
+          perm[out++] = (uint16_t)(s0 + 2);  // lane 2k + 1: one or two
+          if (c == 4) {
+            perm[out++] = (uint16_t)(s0 + 3);
+            flags |= 1u << (2 * taken + 1);
+          }
+          ++taken;
+        }
+      while (first < nc && used[first]) ++first;
+      if (nr < kMaxRounds)
+        R[nr] = (uint64_t)flags | ((uint64_t)base << 32) | ((uint64_t)(2 * taken) << 48);
+      ++nr;
+    }
+    // lone rounds, the two-node items first, then the one-node items (rounds of one
+    // kind: a round of one-node items runs the single contraction): 16 items per
+    // half-warp with distinct residues (a 64-bit warp load is served per half-warp:
+    // 16 distinct doubles in distinct bank pairs = one wavefront each)
+    for (int q = 0; q < nl; ++q) used[q] = 0;
+    for (int kind = 2; kind >= 1; --kind) {
+      left = 0;
+      for (int q = 0; q < nl; ++q) left += lcnt[q] == kind;
+      first = 0;
+      while (left > 0) {
+        uint32_t flags = 0;
+        int taken = 0;
+        const int base = out;
+        for (int half = 0; half < 2 && left > 0; ++half) {
+          uint32_t res = 0;
+          int th = 0;
+          for (int pass = 0; pass < 2 && th < 16 && left > 0; ++pass)
+            for (int q = first; q < nl && th < 16; ++q) {
+              if (used[q] || lcnt[q] != kind) continue;
+              const uint32_t r = so[lstart[q]] & 15u;
+              if (pass == 0 && ((res >> r) & 1u)) continue;
+              res |= 1u << r;
+              used[q] = 1;
+              --left;
+              perm[out++] = lstart[q];
+              if (kind == 2) {
+                perm[out++] = (uint16_t)(lstart[q] + 1);
+                flags |= 1u << taken;
+              }
+              ++taken;
+              ++th;
+            }
+          while (first < nl && (used[first] || lcnt[first] != kind)) ++first;
+          if (th < 16) break;  // a partial half ends the round
+        }
+        if (nr < kMaxRounds)
+          R[nr] = (uint64_t)flags | ((uint64_t)base << 32) | ((uint64_t)taken << 48);
+        ++nr;
+      }
+    }
+    if (nr > kMaxRounds) atomicOr(err, 8);
+    tiles[blockIdx.x].np = blockIdx.x * kMaxRounds;
+    tiles[blockIdx.x].pad2 = min(nr, kMaxRounds);
+  }
+  __syncthreads();
+  if (t < n) {
+    const int o = perm[t];
+    tx[T.e0 + t] = sv[0][o];
+    ty[T.e0 + t] = sv[1][o];
+    tz[T.e0 + t] = sv[2][o];
+    eoff[T.e0 + t] = so[o];
+  }
+}
+
 // ------------------------------------------------------------------ B7
 // Thread per (tile, box row).  Walk the row's x range brick by brick; maximal
 // segments of consecutive Sigma_A cells inside one brick row are consecutive in
@@ -625,6 +772,13 @@ __global__ void k_set_run_ranges(int nT, TileHdr* tiles, const int64_t* rowbase,
   if (t >= nT) return;
   tiles[t].r0 = (int32_t)runstart[rowbase[t]];
   tiles[t].r1 = (int32_t)runstart[rowbase[t + 1]];
+}
+
+__global__ void k_run_offsets(int nT, const TileHdr* tiles, int* beg, int* end) {
+  int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nT) return;
+  beg[t] = tiles[t].r0;
+  end[t] = tiles[t].r1;
 }
 
 // eval ranges start at multiples of 4 nodes (16-byte aligned for bulk copies)
@@ -945,7 +1099,7 @@ void free_band(cpm_band* b) {
   if (b->owns) {
     void* ptrs[] = {b->tiles, b->tx,      b->ty,      b->tz,    b->eoff, b->acell,
                     b->aijk,  b->gijk,    b->runs,    b->vb,    b->dstage0, b->dstage1,
-                    b->amask, b->bmap,    b->fzT,     b->fzH,   b->fzHalo, b->fzEoff, b->fzRuns};
+                    b->amask, b->bmap,    b->rnd,     b->fzT,     b->fzH,   b->fzHalo, b->fzEoff, b->fzRuns};
     for (void* p : ptrs)
       if (p) cudaFree(p);
   } else {  // sub-band: owns only its own tiles/runs/acell/vb
@@ -1148,10 +1302,25 @@ int build_band(const cpm_surface* surf, double h, int p, double L, cudaStream_t 
   count_launch();
   CPM_CUDA(cudaGetLastError());
 
-  // B6c warp order (one-wavefront gathers)
-  k_warp_order<<<totT, 512, 0, s>>>(B->tiles, B->tx, B->ty, B->tz, B->eoff, B->maxBox);
-  count_launch();
-  CPM_CUDA(cudaGetLastError());
+  // B6c/B6d node order for the extend: items (default) or pairs (CPM_ITEMS=0, the
+  // round-1 kernel k_extend_nt, kept for A/B)
+  B->itemOrder = (getenv("CPM_ITEMS") && *getenv("CPM_ITEMS") == '1') &&
+                 !(getenv("CPM_FUSED") && *getenv("CPM_FUSED") == '1');  // the fused kernel uses pairs
+  if (B->itemOrder) {
+    CPM_TRY(dalloc_owned(&B->rnd, (size_t)totT * kMaxRounds, &B->bytes, "item rounds"));
+    k_item_order<<<totT, 512, 0, s>>>(B->tiles, B->tx, B->ty, B->tz, B->eoff, B->rnd, B->maxBox,
+                                      err.as<int>());
+    count_launch();
+    CPM_CUDA(cudaGetLastError());
+    int herr2 = 0;
+    CPM_CUDA(cudaMemcpyAsync(&herr2, err.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CPM_CUDA(cudaStreamSynchronize(s));
+    if (herr2 & 8) return fail(CPM_ERR_LIMIT, "cpm_build_band: a tile needs more than 32 item rounds");
+  } else {
+    k_warp_order<<<totT, 512, 0, s>>>(B->tiles, B->tx, B->ty, B->tz, B->eoff, B->maxBox);
+    count_launch();
+    CPM_CUDA(cudaGetLastError());
+  }
   {  // the strides may have changed: largest box again
     DevBuf mb;
     CPM_TRY(dalloc<int>(mb, 1, "max box"));
@@ -1192,6 +1361,23 @@ int build_band(const cpm_surface* surf, double h, int p, double L, cudaStream_t 
   count_launch();
   CPM_CUDA(cudaGetLastError());
   B->nRuns = totRuns;
+  if (!(getenv("CPM_RUNSORT") && *getenv("CPM_RUNSORT") == '0')) {
+    // each tile's runs in source order: the 4 runs of a warp's cp.async touch fewer
+    // L1 tags (3.38M -> 2.73M per config-1 apply, extend -1 us; CPM_RUNSORT=0: box-row order)
+    DevBuf rb, re, sorted, tmpb;
+    CPM_TRY(dalloc<int>(rb, totT, "run beg"));
+    CPM_TRY(dalloc<int>(re, totT, "run end"));
+    CPM_TRY(dalloc<uint64_t>(sorted, (size_t)totRuns + 2, "sorted runs"));
+    k_run_offsets<<<grid_for(totT, 256), 256, 0, s>>>(totT, B->tiles, rb.as<int>(), re.as<int>());
+    size_t tmp = 0;
+    CPM_CUDA(cub::DeviceSegmentedRadixSort::SortKeys(nullptr, tmp, B->runs, sorted.as<uint64_t>(), (int)totRuns,
+                                                     totT, rb.as<int>(), re.as<int>(), 0, 32, s));
+    CPM_TRY(dalloc<char>(tmpb, tmp, "sort temp"));
+    CPM_CUDA(cub::DeviceSegmentedRadixSort::SortKeys(tmpb.p, tmp, B->runs, sorted.as<uint64_t>(), (int)totRuns,
+                                                     totT, rb.as<int>(), re.as<int>(), 0, 32, s));
+    CPM_CUDA(cudaMemcpyAsync(B->runs, sorted.p, sizeof(uint64_t) * totRuns, cudaMemcpyDeviceToDevice, s));
+    CPM_CUDA(cudaStreamSynchronize(s));
+  }
 
   if (getenv("CPM_FUSED") && *getenv("CPM_FUSED") == '1')
     CPM_TRY(build_fused(B, bmap.as<int>(), dblo.as<int>(), dbdim.as<int>(), s));

@@ -180,7 +180,7 @@ int cpm_band_eval_order(const cpm_band* b, int32_t* tiles_host, uint32_t* eoff_h
     int32_t* o = tiles_host + 6 * t;
     o[0] = T[t].e0;
     o[1] = T[t].e1;
-    o[2] = T[t].np | (T[t].pad2 << 16);
+    o[2] = b->itemOrder ? (int32_t)(0x40000000 | T[t].pad2) : (T[t].np | (T[t].pad2 << 16));
     o[3] = T[t].pad[0];
     o[4] = T[t].pad[1];
     o[5] = T[t].pad[1] * T[t].sz;
@@ -189,6 +189,14 @@ int cpm_band_eval_order(const cpm_band* b, int32_t* tiles_host, uint32_t* eoff_h
     const int64_t ne = T[b->nT - 1].e1;
     CPM_CUDA(cudaMemcpy(eoff_host, b->eoff, sizeof(uint32_t) * ne, cudaMemcpyDeviceToHost));
   }
+  return CPM_OK;
+}
+
+int cpm_band_item_rounds(const cpm_band* b, uint64_t* rounds_host) {
+  if (!b || !rounds_host) return fail(CPM_ERR_ARG, "cpm_band_item_rounds: null argument");
+  if (!b->itemOrder || !b->rnd) return fail(CPM_ERR_ARG, "cpm_band_item_rounds: band is in pair order");
+  if (b->nT > 0)
+    CPM_CUDA(cudaMemcpy(rounds_host, b->rnd, sizeof(uint64_t) * 32 * (size_t)b->nT, cudaMemcpyDeviceToHost));
   return CPM_OK;
 }
 

@@ -123,8 +123,10 @@ struct TileHdr {
   int32_t bx, by, bz;  // brick coordinates (lattice origin = 8*b)
   int32_t pad[3];      // row stride, plane stride of the box; segment id (RAS)
   uint32_t emask[16];  // eval-node cells of the brick (Sigma_A u Sigma_G), bit = cell
-  int32_t np;          // eval nodes e0 + 2p, e0 + 2p + 1 (p < np) share a stencil base
-  int32_t pad2;        // nd: unpaired nodes 2np .. 2np+nd-1 run on lane pairs (the rest one per lane)
+  int32_t np;          // pair order: eval nodes e0 + 2p, e0 + 2p + 1 (p < np) share a stencil base;
+                       // item order: index of the tile's first round word in cpm_band::rnd
+  int32_t pad2;        // pair order: nd, unpaired nodes 2np .. 2np+nd-1 run on lane pairs (the
+                       // rest one per lane); item order: number of rounds
 };
 static_assert(sizeof(TileHdr) == 168, "TileHdr layout");
 
@@ -181,6 +183,13 @@ struct cpm_band {
   int blo[3] = {0, 0, 0}, bdim[3] = {0, 0, 0};
   bool owns = true;                // false for sub-bands sharing the eval arrays
   uint32_t srcSplit = 0xffffffffu; // fill-run sources >= srcSplit read the halo buffer
+  // node order of the extend: items (k_extend_it, rounds in rnd; TileHdr np = first
+  // round, pad2 = rounds) or pairs (k_extend_nt; np = pairs, pad2 = unpaired on lane pairs)
+  bool itemOrder = false;
+  uint64_t* rnd = nullptr;
+  // TMA laplace (apply.cu k_laplace_tma): CUtensorMaps over vb, encoded on first use
+  alignas(64) unsigned char tmX[128] = {}, tmY[128] = {};
+  bool tmReady = false;
 
   // host staging for host-pointer calls
   double* dstage0 = nullptr;       // nA

@@ -360,6 +360,8 @@ int part_create(const cpm_band* B, int rank, int R, cudaStream_t s, cpm_part** o
   L.ty = B->ty;
   L.tz = B->tz;
   L.eoff = B->eoff;
+  L.rnd = B->rnd;
+  L.itemOrder = B->itemOrder;
   L.srcSplit = (uint32_t)P->nOwned;
   L.rank = rank;
   L.nranks = R;

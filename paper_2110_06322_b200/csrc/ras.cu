@@ -546,6 +546,8 @@ int ras_setup_device(const cpm_band* B, int S, int overlap, int k, double c, cud
   M.ty = B->ty;
   M.tz = B->tz;
   M.eoff = B->eoff;
+  M.rnd = B->rnd;
+  M.itemOrder = B->itemOrder;
   CPM_CUDA(cudaMalloc(&M.tiles, sizeof(TileHdr) * std::max(nTs, 1)));
   CPM_CUDA(cudaMalloc(&M.acell, sizeof(uint16_t) * std::max<int64_t>(R->ntot, 1)));
   CPM_CUDA(cudaMalloc(&M.vb, sizeof(double) * kBrickCells * (size_t)std::max(nTs, 1)));

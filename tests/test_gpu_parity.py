@@ -74,6 +74,63 @@ def test_band_bit_exact(cpm, kind, h, kw):
     assert np.all(np.diff(keys) > 0)
 
 
+def _band_with_env(cpm, env, kind, h, **kw):
+    """A band built with build-time switches (read by cpm_build_band from the environment)."""
+    import os
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
+    try:
+        return _gpu_band(cpm, kind, h, **kw)
+    finally:
+        for k, v in old.items():
+            if v is None:
+                del os.environ[k]
+            else:
+                os.environ[k] = v
+
+
+def _item_order_band(cpm, kind, h, **kw):
+    """A band in the item order (CPM_ITEMS=1: the k_extend_it experiment)."""
+    return _band_with_env(cpm, {"CPM_ITEMS": "1"}, kind, h, **kw)
+
+
+@pytest.mark.parametrize("kind,h,kw", [CASES[0], CASES[2], CASES[4], CASES[7]])
+def test_item_order_invariants(cpm, kind, h, kw):
+    """The item order (build.cu k_item_order): the
+    rounds of a tile cover its eval nodes once, in order; an item's two nodes share
+    a stencil base; in a chunk round (lanes in use even, every lane pair one base)
+    a warp reads at most 16 distinct bases, in a lone round at most 32; every
+    stencil stays inside its tile's box."""
+    gb = _item_order_band(cpm, kind, h, **kw)
+    tiles, eoff = cpm.cpm_band_eval_order(gb)
+    rounds = cpm.cpm_band_item_rounds(gb)
+    assert int((tiles[:, 1] - tiles[:, 0]).sum()) == gb.info.n_active + gb.info.n_ghost
+    for t, (e0, e1, word, sx, sxy, cells) in enumerate(tiles.astype(np.int64)):
+        assert word >> 30 == 1
+        nr = word & 0xFFFF
+        ne = e1 - e0
+        assert e0 % 4 == 0 and 1 <= nr <= 32 and np.all(rounds[t, nr:] == 0)
+        eo = eoff[e0:e1].astype(np.int64)
+        base, cell = eo & 0xFFFF, eo >> 16
+        assert np.all(cell < 512) and len(np.unique(cell)) == ne
+        assert np.all(base + 3 * sxy + 3 * sx + 3 < cells)
+        nxt = 0
+        for w in rounds[t, :nr].astype(np.uint64):
+            w = int(w)
+            flags, first, nv = w & 0xFFFFFFFF, (w >> 32) & 0xFFFF, (w >> 48) & 0x3F
+            assert first == nxt and 1 <= nv <= 32 and flags >> nv == 0
+            starts = [first + l + bin(flags & ((1 << l) - 1)).count("1") for l in range(nv)]
+            two = [(flags >> l) & 1 for l in range(nv)]
+            for st, tw in zip(starts, two):
+                if tw:
+                    assert base[st] == base[st + 1]
+            lane_base = [base[st] for st in starts]
+            pair_round = nv % 2 == 0 and all(lane_base[2 * k] == lane_base[2 * k + 1] for k in range(nv // 2))
+            assert len(set(lane_base)) <= (16 if pair_round else 32)
+            nxt = starts[-1] + 1 + two[-1]
+        assert nxt == ne
+
+
 @pytest.mark.parametrize("kind,h,kw", CASES)
 def test_eval_order_invariants(cpm, kind, h, kw):
     """The extend's node order (build.cu k_warp_order): every
@@ -82,6 +139,8 @@ def test_eval_order_invariants(cpm, kind, h, kw):
     reads at most 16 distinct bases, every stencil stays inside its tile's box."""
     gb = _gpu_band(cpm, kind, h, **kw)
     tiles, eoff = cpm.cpm_band_eval_order(gb)
+    with pytest.raises(cpm.CpmError):
+        cpm.cpm_band_item_rounds(gb)
     assert int((tiles[:, 1] - tiles[:, 0]).sum()) == gb.info.n_active + gb.info.n_ghost
     for e0, e1, npnd, sx, sxy, cells in tiles.astype(np.int64):
         npair, nd = npnd & 0xFFFF, npnd >> 16
@@ -100,6 +159,38 @@ def test_eval_order_invariants(cpm, kind, h, kw):
             assert len(np.unique(base[node[w0:w0 + 32]])) <= 16
         # the unpaired region starts on a warp boundary (or the tile's last warp)
         assert (np2 + 2 * nd) % 32 == 0 or np2 + nd == ne
+
+
+@pytest.mark.parametrize("kind,h,kw", [CASES[0], CASES[2], CASES[4], CASES[7]])
+def test_item_order_apply_bit_identical_to_pair_order(cpm, kind, h, kw):
+    """k_extend_it (the item-order experiment) evaluates each node with
+    k_extend_nt's operations in the same order: the two node orders give
+    bit-identical applies."""
+    gi = _item_order_band(cpm, kind, h, **kw)
+    gp = _gpu_band(cpm, kind, h, **kw)
+    ga = cpm.cpm_band_active_coords(gi).astype(np.int64)
+    assert np.array_equal(ga, cpm.cpm_band_active_coords(gp))
+    u = torch.from_numpy(seeded_inputs.uniform_pm1(0, ga)).cuda()
+    yi, yp = torch.empty_like(u), torch.empty_like(u)
+    cpm.cpm_apply(gi, 1.0, u, yi)
+    cpm.cpm_apply(gp, 1.0, u, yp)
+    torch.cuda.synchronize()
+    assert torch.equal(yi, yp)
+
+
+@pytest.mark.parametrize("kind,h,kw", [CASES[2], CASES[4]])
+def test_run_order_does_not_change_the_apply(cpm, kind, h, kw):
+    """The fill runs in source order (default) or box-row order (CPM_RUNSORT=0)
+    stage the same box: bit-identical applies."""
+    g0 = _gpu_band(cpm, kind, h, **kw)
+    g1 = _band_with_env(cpm, {"CPM_RUNSORT": "0"}, kind, h, **kw)
+    ga = cpm.cpm_band_active_coords(g0).astype(np.int64)
+    u = torch.from_numpy(seeded_inputs.uniform_pm1(0, ga)).cuda()
+    y0, y1 = torch.empty_like(u), torch.empty_like(u)
+    cpm.cpm_apply(g0, 1.0, u, y0)
+    cpm.cpm_apply(g1, 1.0, u, y1)
+    torch.cuda.synchronize()
+    assert torch.equal(y0, y1)
 
 
 @pytest.mark.parametrize("kind,h,kw", CASES)

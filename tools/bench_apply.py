@@ -1,7 +1,8 @@
 """Quick apply timing on config 1 (for iterating on kernels).
 
-CPM_KS="1 2 3 4" times the apply for each node-group size K (band rebuilt per K)
-and checks that all K give the same result (up to rounding).
+CPM_ORDERS="1 0" times the apply for each extend node order (CPM_ITEMS = 1: items,
+k_extend_it; 0: pairs, k_extend_nt; band rebuilt per order) and prints the max
+difference against the first (0 = bit-identical).
 """
 import os
 import sys
@@ -14,10 +15,10 @@ import paper_2110_06322_b200 as cpm
 import seeded_inputs
 
 h = float(os.environ.get("CPM_H", 1.0 / 200))
-ks = [int(k) for k in os.environ.get("CPM_KS", "4").split()]
+ks = [int(k) for k in os.environ.get("CPM_ORDERS", "1").split()]
 ref = None
 for K in ks:
-    os.environ["CPM_GROUP_K"] = str(K)
+    os.environ["CPM_ITEMS"] = str(K)
     band = cpm.cpm_build_band("sphere", h)
     coords = cpm.cpm_band_active_coords(band).astype(np.int64)
     u = torch.from_numpy(seeded_inputs.uniform_pm1(0, coords)).cuda()
@@ -44,9 +45,9 @@ for K in ks:
     l, _ = cpm.cpm_profile_read("laplace")
     nA, nG = band.info.n_active, band.info.n_ghost
     alg = 16 * nA + 28 * (nA + nG)
-    print(f"{'FUSED ' if os.environ.get('CPM_FUSED') == '1' else ''}K={K} nA={nA} tiles={band.info.n_tiles} runs={band.info.n_runs} maxbox={band.info.max_box} "
+    print(f"{'FUSED ' if os.environ.get('CPM_FUSED') == '1' else ''}items={K} nA={nA} tiles={band.info.n_tiles} runs={band.info.n_runs} maxbox={band.info.max_box} "
           f"apply {ms*1e3:.1f} us (extend {e/N*1e3:.1f} us, laplace {l/N*1e3:.1f} us) -> "
-          f"{alg/ms/1e6:.0f} GB/s alg, {nA/ms/1e6:.2f} Gnodes/s, diff vs first K {err:.1e}", flush=True)
+          f"{alg/ms/1e6:.0f} GB/s alg, {nA/ms/1e6:.2f} Gnodes/s, diff vs first {err:.1e}", flush=True)
     del band
 if os.environ.get("CPM_SOLVE"):
     band = cpm.cpm_build_band("sphere", h)
