@@ -360,7 +360,7 @@ __global__ void __launch_bounds__(512) k_sort_tile(const TileHdr* tiles, double*
 // are decoded from the current offsets; so[] (sorted by offset) is re-encoded.
 // Called by all threads of a 512-thread CTA.
 __device__ void balance_strides(const TileHdr& T, TileHdr* hdr, uint32_t* so, int n, int boxCap,
-                                unsigned long long& best) {
+                                unsigned long long& best, bool exact = false) {
   const int t = threadIdx.x;
   if (t == 0) best = ~0ull;
   __syncthreads();
@@ -371,7 +371,42 @@ __device__ void balance_strides(const TileHdr& T, TileHdr* hdr, uint32_t* so, in
     int cnt[16];
 #pragma unroll
     for (int r = 0; r < 16; ++r) cnt[r] = 0;
-    if (t < 256) {
+    if (t < 256 && exact) {
+      // the gather wavefronts the pair dealing needs with these strides: equal-base
+      // groups give c/2 pairs on one address (broadcast) and c % 2 single; per
+      // residue r, pair addresses pc[r] and singles sc[r]; pair warps cost
+      // >= max(ceil(P/16), max pc), single half-warps >= max(ceil(S/16), max sc)
+      int sc[16], P = 0, S = 0;
+#pragma unroll
+      for (int r = 0; r < 16; ++r) sc[r] = 0;
+      for (int i = 0; i < n;) {
+        const int o = so[i] & 0xffff;
+        int j = i + 1;
+        while (j < n && (int)(so[j] & 0xffff) == o) ++j;
+        const int dz = o / pxy0, rem = o - dz * pxy0, dy = rem / px0, dx = rem - dy * px0;
+        const int r = (dx + px * dy + pxy * dz) & 15, c = j - i;
+        if (c >= 2) {
+          cnt[r] += (c / 2 + 15) / 16;
+          P += c / 2;
+        }
+        if (c & 1) {
+          sc[r]++;
+          ++S;
+        }
+        i = j;
+      }
+      int mp = 0, ms = 0;
+#pragma unroll
+      for (int r = 0; r < 16; ++r) {
+        mp = max(mp, cnt[r]);
+        ms = max(ms, sc[r]);
+      }
+      const int cost = max((P + 15) / 16, mp) + max((S + 15) / 16, ms);
+      const unsigned cells = (unsigned)(pxy * T.sz);
+      if (cells <= (unsigned)boxCap)
+        atomicMin(&best, ((unsigned long long)min(cost, 1023) << 40) | ((unsigned long long)cells << 8) |
+                             (unsigned long long)t);
+    } else if (t < 256) {
       for (int i = 0; i < n; ++i) {
         const int o = so[i] & 0xffff;
         if (i > 0 && o == (int)(so[i - 1] & 0xffff)) continue;  // distinct bases (sorted input)
@@ -406,6 +441,48 @@ __device__ void balance_strides(const TileHdr& T, TileHdr* hdr, uint32_t* so, in
   __syncthreads();
 }
 
+// Deal n items (node indices, sorted by stencil-box offset) into groups of 16
+// whose offsets are distinct mod 16 where the residue counts allow it: each group
+// takes the head item of the residue class with the most items left among the
+// classes it has not used yet (so the classes drain evenly and conflicts are left
+// for the last groups only), together with the following items of that class with
+// the same offset (one address: a broadcast, free); when every class is used, the
+// fullest classes again.  Thread-0 code; out receives the dealt order.
+__device__ void deal16(const uint16_t* item, int n, const uint32_t* so, uint16_t* bk, uint16_t* out) {
+  int cnt[16], head[16];
+  for (int r = 0; r < 16; ++r) cnt[r] = 0;
+  for (int i = 0; i < n; ++i) ++cnt[so[item[i]] & 15u];
+  int st = 0;
+  for (int r = 0; r < 16; ++r) {
+    head[r] = st;
+    st += cnt[r];
+  }
+  {
+    int pos[16];
+    for (int r = 0; r < 16; ++r) pos[r] = head[r];
+    for (int i = 0; i < n; ++i) bk[pos[so[item[i]] & 15u]++] = item[i];  // stable: offset order kept
+  }
+  int left = n, k = 0;
+  while (left > 0) {
+    int taken = 0;
+    uint32_t used = 0;
+    while (taken < 16 && left > 0) {
+      int best = -1;
+      for (int pass = 0; pass < 2 && best < 0; ++pass)
+        for (int r = 0; r < 16; ++r)
+          if (cnt[r] > 0 && (pass == 1 || !((used >> r) & 1u)) && (best < 0 || cnt[r] > cnt[best])) best = r;
+      const uint32_t o = so[bk[head[best]]] & 0xffffu;
+      do {
+        out[k++] = bk[head[best]++];
+        --cnt[best];
+        --left;
+        ++taken;
+      } while (taken < 16 && cnt[best] > 0 && (so[bk[head[best]]] & 0xffffu) == o);
+      used |= 1u << best;
+    }
+  }
+}
+
 // ------------------------------------------------------------------ B6c
 // Warp order: k_extend_nt gives the tile's nodes 32 at a time to the lanes of a
 // warp.  An 8-byte shared-memory load of a warp costs ONE wavefront when every
@@ -418,10 +495,10 @@ __device__ void balance_strides(const TileHdr& T, TileHdr* hdr, uint32_t* so, in
 // 16 per half-warp by the same rule.
 // One CTA per tile, thread 0 plans.
 __global__ void __launch_bounds__(512) k_warp_order(TileHdr* tiles, double* tx, double* ty,
-                                                    double* tz, uint32_t* eoff, int boxCap) {
+                                                    double* tz, uint32_t* eoff, int boxCap, int newdeal) {
   __shared__ double sv[3][512];
   __shared__ uint32_t so[512];
-  __shared__ uint16_t perm[512], pfirst[256], single[512];
+  __shared__ uint16_t perm[512], pfirst[256], single[512], bk[512], dealt[512];
   __shared__ uint8_t pused[512];
   __shared__ int npair, ndup;
   __shared__ unsigned long long best;
@@ -433,7 +510,7 @@ __global__ void __launch_bounds__(512) k_warp_order(TileHdr* tiles, double* tx, 
     sv[2][t] = tz[T.e0 + t];
     so[t] = eoff[T.e0 + t];
   }
-  balance_strides(T, tiles + blockIdx.x, so, n, boxCap, best);
+  balance_strides(T, tiles + blockIdx.x, so, n, boxCap, best, newdeal >= 2);
   if (t == 0) {
     int np = 0, ns = 0;
     for (int i = 0; i < n;) {  // groups of equal base -> pairs + a singleton
@@ -453,9 +530,17 @@ __global__ void __launch_bounds__(512) k_warp_order(TileHdr* tiles, double* tx, 
     // last pair warp on both lanes of a lane pair): pairs first
     int out = 0, taken = 0, nd = 0;
     uint32_t res = 0;
-    uint16_t toff[16];
-    for (int q = 0; q < np; ++q) pused[q] = 0;
-    {
+    if (newdeal) {
+      deal16(pfirst, np, so, bk, dealt);
+      for (int q = 0; q < np; ++q) {
+        perm[out++] = dealt[q];
+        perm[out++] = (uint16_t)(dealt[q] + 1);
+      }
+      taken = np & 15;
+      for (int q = np - taken; q < np; ++q) res |= 1u << (so[dealt[q]] & 15u);
+    } else {
+      uint16_t toff[16];
+      for (int q = 0; q < np; ++q) pused[q] = 0;
       int first = 0, left = np;
       while (left > 0) {
         for (int pass = 0; pass < 2 && taken < 16; ++pass) {  // compatible first, then any
@@ -501,26 +586,34 @@ __global__ void __launch_bounds__(512) k_warp_order(TileHdr* tiles, double* tx, 
     }
     // the other unpaired nodes one per lane, 16 per half-warp with distinct residues
     // (16 distinct doubles of a half-warp in distinct bank pairs: one wavefront)
-    taken = 0;
-    res = 0;
-    int first = 0;
-    while (sleft > 0) {
-      for (int pass = 0; pass < 2 && taken < 16 && sleft > 0; ++pass) {
-        for (int q = first; q < ns && taken < 16; ++q) {
-          if (pused[q]) continue;
-          const uint32_t r = so[single[q]] & 15u;
-          if (pass == 0 && ((res >> r) & 1u)) continue;
-          res |= 1u << r;
-          ++taken;
-          pused[q] = 1;
-          --sleft;
-          perm[out++] = single[q];
+    if (newdeal) {
+      int nl = 0;
+      for (int q = 0; q < ns; ++q)
+        if (!pused[q]) dealt[nl++] = single[q];
+      deal16(dealt, nl, so, bk, perm + out);
+      out += nl;
+    } else {
+      taken = 0;
+      res = 0;
+      int first = 0;
+      while (sleft > 0) {
+        for (int pass = 0; pass < 2 && taken < 16 && sleft > 0; ++pass) {
+          for (int q = first; q < ns && taken < 16; ++q) {
+            if (pused[q]) continue;
+            const uint32_t r = so[single[q]] & 15u;
+            if (pass == 0 && ((res >> r) & 1u)) continue;
+            res |= 1u << r;
+            ++taken;
+            pused[q] = 1;
+            --sleft;
+            perm[out++] = single[q];
+          }
         }
-      }
-      while (first < ns && pused[first]) ++first;
-      if (taken == 16) {
-        taken = 0;
-        res = 0;
+        while (first < ns && pused[first]) ++first;
+        if (taken == 16) {
+          taken = 0;
+          res = 0;
+        }
       }
     }
     ndup = nd;
@@ -1317,7 +1410,10 @@ int build_band(const cpm_surface* surf, double h, int p, double L, cudaStream_t 
     CPM_CUDA(cudaStreamSynchronize(s));
     if (herr2 & 8) return fail(CPM_ERR_LIMIT, "cpm_build_band: a tile needs more than 32 item rounds");
   } else {
-    k_warp_order<<<totT, 512, 0, s>>>(B->tiles, B->tx, B->ty, B->tz, B->eoff, B->maxBox);
+    // CPM_DEAL=0: the round-1 greedy dealing and residue balance; 1: class-draining
+    // dealing; 2 (default): that dealing with strides chosen by its wavefront bound
+    const int newdeal = getenv("CPM_DEAL") ? atoi(getenv("CPM_DEAL")) : 2;
+    k_warp_order<<<totT, 512, 0, s>>>(B->tiles, B->tx, B->ty, B->tz, B->eoff, B->maxBox, newdeal);
     count_launch();
     CPM_CUDA(cudaGetLastError());
   }
