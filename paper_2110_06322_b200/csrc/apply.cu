@@ -62,7 +62,6 @@ __device__ __forceinline__ void cp_wait() {
 // few distinct addresses (broadcast).  u is read with an evict-last L2 policy
 // and vb written with one, so both stay resident in L2 for k_laplace.
 constexpr int kNtThreads = 128;
-constexpr int kNtPre = 3;  // slots per thread whose node offsets are prefetched
 
 __device__ __forceinline__ uint64_t policy_evict_last() {
   uint64_t p;
@@ -146,8 +145,8 @@ __device__ __forceinline__ void contract_node(const double (&tn)[3], uint32_t eo
   if (write) st_hint(out + (eo >> 16), acc, pol);
 }
 
-template <bool ZERO>
-__global__ void __launch_bounds__(kNtThreads, 8)
+template <bool ZERO, int MINB = 8, int kNtPre = 3>
+__global__ void __launch_bounds__(kNtThreads, MINB)
     k_extend_nt(const TileHdr* __restrict__ tiles, int boxCells, int descCap,
                 const uint64_t* __restrict__ runs, const double* __restrict__ u,
                 const double* __restrict__ uh, uint32_t split, const double* __restrict__ tx,
@@ -751,21 +750,22 @@ int extend_tiles(const cpm_band* b, const double* u, const double* uh, cudaStrea
                  int t0, int t1) {
   if (t1 <= t0) return CPM_OK;
   const int pfd = prefetch_distance();
-  const int descCap = 512;
+  // descriptors staged per round: 256 (2 KB) lets 9 CTAs per SM fit next to the largest config-1 box
+  static const int descCap = getenv("CPM_DESC_CAP") ? atoi(getenv("CPM_DESC_CAP")) : 256;
   // CPM_EXT_SMEM_PAD (bytes, experiment): extra dynamic shared memory per CTA, to
   // measure the extend's sensitivity to resident CTAs per SM
   static const size_t smpad = getenv("CPM_EXT_SMEM_PAD") ? (size_t)atol(getenv("CPM_EXT_SMEM_PAD")) : 0;
   const size_t smem = (size_t)b->maxBox * 8 + (size_t)descCap * 8 + smpad;
   ProfScope ps(K_EXTEND, s);
-#define CPM_EXTNT(Z)                                                                         \
+#define CPM_EXTNT(Z, MB, PRE)                                                                \
   do {                                                                                       \
     static bool attr = false;                                                                \
     if (!attr) {                                                                             \
-      CPM_CUDA(cudaFuncSetAttribute(k_extend_nt<Z>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+      CPM_CUDA(cudaFuncSetAttribute(k_extend_nt<Z, MB, PRE>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                                     227 * 1024));                                            \
       attr = true;                                                                           \
     }                                                                                        \
-    CPM_CUDA(launch_pdl_l2(vb_window(b), k_extend_nt<Z>, dim3((unsigned)(t1 - t0)), dim3(kNtThreads), smem, s, \
+    CPM_CUDA(launch_pdl_l2(vb_window(b), k_extend_nt<Z, MB, PRE>, dim3((unsigned)(t1 - t0)), dim3(kNtThreads), smem, s, \
                         b->tiles, (int)b->maxBox, descCap, (const uint64_t*)b->runs, u, uh,     \
                         (uint32_t)b->srcSplit, (const double*)b->tx, (const double*)b->ty,      \
                         (const double*)b->tz, (const uint32_t*)b->eoff, b->vb, skip, pfd, t0, t1)); \
@@ -794,7 +794,17 @@ int extend_tiles(const cpm_band* b, const double* u, const double* uh, cudaStrea
       if (b->zeroFill) CPM_EXTIT(true, 6); else CPM_EXTIT(false, 6);
     }
   } else {
-    if (b->zeroFill) CPM_EXTNT(true); else CPM_EXTNT(false);
+    // default: 56 registers (9 CTAs per SM), 2 slots' offsets prefetched (config 1:
+    // 119.4 -> 117.1 us against 64 registers / 8 CTAs / 3 slots); CPM_NT_CFG=0: the
+    // latter, 2: 9 CTAs with 3 slots (118.9 us)
+    static const int cfg = getenv("CPM_NT_CFG") ? atoi(getenv("CPM_NT_CFG")) : 1;
+    if (cfg == 0) {
+      if (b->zeroFill) CPM_EXTNT(true, 8, 3); else CPM_EXTNT(false, 8, 3);
+    } else if (cfg == 2) {
+      if (b->zeroFill) CPM_EXTNT(true, 9, 3); else CPM_EXTNT(false, 9, 3);
+    } else {
+      if (b->zeroFill) CPM_EXTNT(true, 9, 2); else CPM_EXTNT(false, 9, 2);
+    }
   }
 #undef CPM_EXTNT
 #undef CPM_EXTIT
