@@ -145,7 +145,7 @@ __device__ __forceinline__ void contract_node(const double (&tn)[3], uint32_t eo
   if (write) st_hint(out + (eo >> 16), acc, pol);
 }
 
-template <bool ZERO, int MINB = 8, int kNtPre = 3>
+template <bool ZERO, int MINB = 8, int kNtPre = 3, int FILL = 1>
 __global__ void __launch_bounds__(kNtThreads, MINB)
     k_extend_nt(const TileHdr* __restrict__ tiles, int boxCells, int descCap,
                 const uint64_t* __restrict__ runs, const double* __restrict__ u,
@@ -183,7 +183,7 @@ __global__ void __launch_bounds__(kNtThreads, MINB)
     const int nbox = sxy * T->sz;
     for (int c = tid; c < nbox; c += kNtThreads) box[c] = 0.0;
   }
-  const int g = tid >> 3, l = tid & 7;
+  const int g = tid >> 3, l = tid & 7, g4 = tid >> 2, l4 = tid & 3;
   int nr = min(descCap, r1 - r0);
   for (int r = tid; r < nr; r += kNtThreads) cp_async8_hint(desc + r, runs + r0 + r, pfirst);
   cp_commit();
@@ -200,13 +200,27 @@ __global__ void __launch_bounds__(kNtThreads, MINB)
     }
     cp_wait<0>();
     __syncthreads();  // descriptors landed (and the ZERO clear done)
-    for (int r = g; r < nr; r += kNtThreads / 8) {
-      const uint64_t d = desc[r];
-      const uint32_t src = (uint32_t)d, dst = (uint32_t)(d >> 32) & 0xffffu,
-                     len = (uint32_t)(d >> 48) & 0xffu;
-      if (l < len) {
+    if (FILL == 1) {
+      // 4 lanes per run, cells l and l + 4: 8 runs per warp iteration (the round-1 8 lanes
+      // per run left half the lanes idle on runs of ~4 cells and doubled the loop's
+      // issue: extend 117.1 -> 108.5 us at config 1)
+      for (int r = g4; r < nr; r += kNtThreads / 4) {
+        const uint64_t d = desc[r];
+        const uint32_t src = (uint32_t)d, dst = (uint32_t)(d >> 32) & 0xffffu,
+                       len = (uint32_t)(d >> 48) & 0xffu;
         const double* gsrc = src >= split ? uh + (src - split) : u + src;  // runs never straddle split
-        cp_async8_hint(box + dst + l, gsrc + l, plast);
+        if (l4 < len) cp_async8_hint(box + dst + l4, gsrc + l4, plast);
+        if (l4 + 4 < len) cp_async8_hint(box + dst + l4 + 4, gsrc + l4 + 4, plast);
+      }
+    } else {
+      for (int r = g; r < nr; r += kNtThreads / 8) {
+        const uint64_t d = desc[r];
+        const uint32_t src = (uint32_t)d, dst = (uint32_t)(d >> 32) & 0xffffu,
+                       len = (uint32_t)(d >> 48) & 0xffu;
+        if (l < len) {
+          const double* gsrc = src >= split ? uh + (src - split) : u + src;  // runs never straddle split
+          cp_async8_hint(box + dst + l, gsrc + l, plast);
+        }
       }
     }
     cp_commit();
@@ -757,15 +771,15 @@ int extend_tiles(const cpm_band* b, const double* u, const double* uh, cudaStrea
   static const size_t smpad = getenv("CPM_EXT_SMEM_PAD") ? (size_t)atol(getenv("CPM_EXT_SMEM_PAD")) : 0;
   const size_t smem = (size_t)b->maxBox * 8 + (size_t)descCap * 8 + smpad;
   ProfScope ps(K_EXTEND, s);
-#define CPM_EXTNT(Z, MB, PRE)                                                                \
+#define CPM_EXTNT(Z, MB, PRE, F4)                                                              \
   do {                                                                                       \
     static bool attr = false;                                                                \
     if (!attr) {                                                                             \
-      CPM_CUDA(cudaFuncSetAttribute(k_extend_nt<Z, MB, PRE>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+      CPM_CUDA(cudaFuncSetAttribute(k_extend_nt<Z, MB, PRE, F4>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                                     227 * 1024));                                            \
       attr = true;                                                                           \
     }                                                                                        \
-    CPM_CUDA(launch_pdl_l2(vb_window(b), k_extend_nt<Z, MB, PRE>, dim3((unsigned)(t1 - t0)), dim3(kNtThreads), smem, s, \
+    CPM_CUDA(launch_pdl_l2(vb_window(b), k_extend_nt<Z, MB, PRE, F4>, dim3((unsigned)(t1 - t0)), dim3(kNtThreads), smem, s, \
                         b->tiles, (int)b->maxBox, descCap, (const uint64_t*)b->runs, u, uh,     \
                         (uint32_t)b->srcSplit, (const double*)b->tx, (const double*)b->ty,      \
                         (const double*)b->tz, (const uint32_t*)b->eoff, b->vb, skip, pfd, t0, t1)); \
@@ -798,12 +812,15 @@ int extend_tiles(const cpm_band* b, const double* u, const double* uh, cudaStrea
     // 119.4 -> 117.1 us against 64 registers / 8 CTAs / 3 slots); CPM_NT_CFG=0: the
     // latter, 2: 9 CTAs with 3 slots (118.9 us)
     static const int cfg = getenv("CPM_NT_CFG") ? atoi(getenv("CPM_NT_CFG")) : 1;
+    static const int fill = getenv("CPM_FILL") ? atoi(getenv("CPM_FILL")) : 1;  // 0: 8 lanes per run
     if (cfg == 0) {
-      if (b->zeroFill) CPM_EXTNT(true, 8, 3); else CPM_EXTNT(false, 8, 3);
+      if (b->zeroFill) CPM_EXTNT(true, 8, 3, 0); else CPM_EXTNT(false, 8, 3, 0);
     } else if (cfg == 2) {
-      if (b->zeroFill) CPM_EXTNT(true, 9, 3); else CPM_EXTNT(false, 9, 3);
+      if (b->zeroFill) CPM_EXTNT(true, 9, 3, 0); else CPM_EXTNT(false, 9, 3, 0);
+    } else if (fill == 1) {
+      if (b->zeroFill) CPM_EXTNT(true, 9, 2, 1); else CPM_EXTNT(false, 9, 2, 1);
     } else {
-      if (b->zeroFill) CPM_EXTNT(true, 9, 2); else CPM_EXTNT(false, 9, 2);
+      if (b->zeroFill) CPM_EXTNT(true, 9, 2, 0); else CPM_EXTNT(false, 9, 2, 0);
     }
   }
 #undef CPM_EXTNT

@@ -1412,6 +1412,8 @@ int build_band(const cpm_surface* surf, double h, int p, double L, cudaStream_t 
   } else {
     // CPM_DEAL=0: the round-1 greedy dealing and residue balance; 1: class-draining
     // dealing; 2 (default): that dealing with strides chosen by its wavefront bound
+    // (restricting the row stride to 4 mod 8 for a conflict-free fill of consecutive
+    // rows was measured: fill wavefronts 3.15M -> 2.86M, gathers 15.6M -> 16.1M, +0.8 us)
     const int newdeal = getenv("CPM_DEAL") ? atoi(getenv("CPM_DEAL")) : 2;
     k_warp_order<<<totT, 512, 0, s>>>(B->tiles, B->tx, B->ty, B->tz, B->eoff, B->maxBox, newdeal);
     count_launch();
