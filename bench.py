@@ -114,7 +114,7 @@ KERNELS = ["extend", "laplace", "mdot", "cgs_update", "cgs_final", "axpy", "othe
 
 def _traffic():
     """ncu DRAM bytes (read + write) per apply, from the committed capture summary."""
-    p = os.path.join(ROOT, "profiles", "r02_traffic.json")
+    p = os.path.join(ROOT, "profiles", "r02_traffic_v3.json")
     try:
         d = json.load(open(p))
         return float(d["apply_dram_bytes"])
@@ -456,16 +456,16 @@ def run_mine(args):
             "solve": {"seconds_median": solve_med_ms / 1e3, "iterations": stats[-1].iterations,
                       "converged": stats[-1].converged, "resid_true_rel": stats[-1].resid_true / stats[-1].bnorm},
             "build_band_s": build_s,
-            "roofline": {"kernel": "apply = k_extend_nt + k_laplace (one apply, the metric's unit)",
+            "roofline": {"kernel": "apply = k_extend_nt + k_laplace_tma (one apply, the metric's unit)",
                          "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                          "alg_bytes_per_apply": alg_bytes,
                          "apply_ms": mean_apply_s * 1e3,
                          "extend_ms": ext_ms / max(ext_n, 1), "laplace_ms": lap_ms / max(lap_n, 1),
-                         "note": "the extend is bound by its l1tex issue (64 shared-memory gathers per node "
+                         "note": "the extend is bound by its l1tex data path (64 shared-memory gathers per node "
                                  "slot, the cp.async box fill, scattered E u stores: DESIGN.md §Kernels, "
-                                 "profiles/r02_extend_sass_l1tex.txt); traffic = ncu DRAM bytes per apply "
-                                 "(profiles/r02_traffic.json)"},
+                                 "profiles/r02_ncu_v3.txt); traffic = ncu DRAM bytes per apply "
+                                 "(profiles/r02_traffic_v3.json)"},
             "roofline_solve": {"kernel": "Krylov passes of the solve (k_dcgs_dots + k_dcgs_update), "
                                          "the largest share of a step",
                                "bound": "hbm", "achieved": kry_gbs, "peak": peak, "unit": "GB/s",
