@@ -56,6 +56,15 @@ void count_launch();
 // launched with launch_pdl calls pdl_wait() first.  CPM_PDL=0 disables it.
 bool pdl_enabled();
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+// Early trigger, called right after pdl_wait() by the Krylov reduction passes only:
+// the update pass that follows may launch once every CTA of the reduction pass has
+// started, and loads its first tile (Q columns, u_j, z: written two or more kernels
+// back) before its own pdl_wait(), while the reduction's completing block runs the
+// GMRES step epilogue (config-1 solve 0.887 -> 0.883 s).  Its pdl_wait() still waits
+// for this grid's completion and memory flush.  Triggering in every per-step kernel
+// (extend, laplace, update too) was measured: solve 1.05 s — the waiting dependents'
+// CTAs cost the draining grids more than their early start saves.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
                               cudaStream_t s, Args&&... args) {

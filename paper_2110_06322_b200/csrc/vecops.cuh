@@ -333,6 +333,7 @@ static __global__ void __launch_bounds__(TB) k_dcgs_dots(Seg S, int k, const dou
                                                          const int* __restrict__ skip, int ns,
                                                          Epi epi = Epi()) {
   pdl_wait();
+  pdl_trigger();
   if (skip && *skip) return;
   extern __shared__ double smp[];  // ns stages of k + 1 columns (Q_0 .. Q_{j-1}, u_j, z)
   __shared__ bool last;
@@ -476,6 +477,7 @@ static __global__ void __launch_bounds__(256) k_dcgs_dots_bulk(Seg S, int k, con
                                                                Epi epi = Epi()) {
   constexpr int TB = 256, SVB = TB + 4;
   pdl_wait();
+  pdl_trigger();
   if (skip && *skip) return;
   extern __shared__ __align__(16) double smp[];
   __shared__ __align__(8) uint64_t full[4];
@@ -596,6 +598,7 @@ static __global__ void __launch_bounds__(256, 2) k_dcgs_dots_tma(Seg S, int k, c
                                                                   int ns, Epi epi = Epi()) {
   constexpr int TB = 256, NW = TB / 32, TE = 128;
   pdl_wait();
+  pdl_trigger();
   if (skip && *skip) return;
   extern __shared__ __align__(16) double smt[];
   __shared__ __align__(8) uint64_t full[8];
@@ -695,6 +698,7 @@ static __global__ void __launch_bounds__(256, MINB) k_dcgs_dots_direct(
     int pld, double* out, int ldo, unsigned* counters, const int* __restrict__ skip, Epi epi = Epi()) {
   constexpr int TB = 256, NW = TB / 32, TE = 128;
   pdl_wait();
+  pdl_trigger();
   if (skip && *skip) return;
   __shared__ bool last;
   const int s = blockIdx.x / S.gps, lb = blockIdx.x % S.gps;
@@ -889,34 +893,50 @@ static __global__ void __launch_bounds__(TB, MINB) k_dcgs_update_reg(Seg S, int 
                                                                   const double* __restrict__ coef0,
                                                                   int ldc, int64_t cstride,
                                                                   const int* __restrict__ skip) {
-  pdl_wait();
-  if (skip && *skip) return;
   __shared__ double cb[KMAX], ce[KMAX];
   const int s = blockIdx.x / S.gps, lb = blockIdx.x % S.gps;
   const int64_t o0 = S.off[s], n = S.off[s + 1] - o0;
-  const double* coef = coef0 + (size_t)s * cstride;  // this segment's coefficients
   const int tid = threadIdx.x;
   const int j = k - 1;
+  // tiles from the block's last to its first: the reduction pass before this one
+  // ended on the high tiles, which are still in L2 (each element is independent)
+  const int64_t stride = (int64_t)S.gps * TB, tf = (int64_t)lb * TB;
+  const int64_t tl = tf < n ? tf + (n - 1 - tf) / stride * stride : tf - stride;
+  // the first tile's Q columns, u_j and z are loaded before pdl_wait(): they were
+  // written two or more kernels back (the apply before the reduction pass this
+  // kernel follows, the update passes before it), so only the coefficients wait
+  double q[KMAX], uv = 0.0, zv = 0.0;
+  {
+    const int64_t e = tl + tid;
+    if (tl >= tf && e < n) {
+      const double* p = V + o0 + e;
+#pragma unroll
+      for (int i = 0; i < KMAX; ++i)
+        if (i < j) q[i] = __ldcg(p + (size_t)i * ldv);
+      uv = __ldcg(p + (size_t)j * ldv);
+      zv = __ldcg(z + o0 + e);
+    }
+  }
+  pdl_wait();
+  if (skip && *skip) return;
+  const double* coef = coef0 + (size_t)s * cstride;  // this segment's coefficients
   for (int i = tid; i < j; i += TB) {
     cb[i] = coef[i];
     ce[i] = coef[ldc + i];
   }
   const double rinv = 1.0 / coef[2 * ldc], mu = coef[2 * ldc + 1];
   __syncthreads();
-  // tiles from the block's last to its first: the reduction pass before this one
-  // ended on the high tiles, which are still in L2 (each element is independent)
-  const int64_t stride = (int64_t)S.gps * TB, tf = (int64_t)lb * TB;
-  const int64_t tl = tf < n ? tf + (n - 1 - tf) / stride * stride : tf - stride;
   for (int64_t t0 = tl; t0 >= tf; t0 -= stride) {
     const int64_t e = t0 + tid;
     if (e >= n) continue;
-    const double* p = V + o0 + e;
-    double q[KMAX];
+    if (t0 != tl) {
+      const double* p = V + o0 + e;
 #pragma unroll
-    for (int i = 0; i < KMAX; ++i)
-      if (i < j) q[i] = __ldcg(p + (size_t)i * ldv);
-    const double uv = __ldcg(p + (size_t)j * ldv);
-    const double zv = __ldcg(z + o0 + e);
+      for (int i = 0; i < KMAX; ++i)
+        if (i < j) q[i] = __ldcg(p + (size_t)i * ldv);
+      uv = __ldcg(p + (size_t)j * ldv);
+      zv = __ldcg(z + o0 + e);
+    }
     double sb0 = 0.0, sb1 = 0.0, se0 = 0.0, se1 = 0.0;
 #pragma unroll
     for (int i = 0; i + 1 < KMAX; i += 2) {
