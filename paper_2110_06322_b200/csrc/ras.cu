@@ -243,7 +243,7 @@ __global__ void k_gather(int64_t n, const int64_t* gidx, const double* r, const 
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t g = gidx[i];
-    x[i] = g < nown ? r[g] : rh[g - nown];
+    x[i] = g < 0 ? 0.0 : (g < nown ? r[g] : rh[g - nown]);  // g < 0: a segment's pad entry
   }
 }
 
@@ -420,7 +420,9 @@ inline int g1(int64_t n) { return (int)std::max<int64_t>(1, std::min<int64_t>((n
 struct RasImpl {
   cpm_band mb;            // the multi-band (owns=false): sub-tiles, runs, local acell, vb
   int S = 0, k = 0;
-  int64_t ntot = 0;
+  int64_t ntot = 0;                 // concatenated segments, pads included
+  int64_t nmem = 0;                 // members (without the pads)
+  int aligned = 0;                  // segment starts are multiples of 32 elements
   std::vector<int64_t> off_h;  // S + 1
   int64_t* off = nullptr;      // device S + 1
   int64_t* gidx = nullptr;     // Ntot
@@ -520,13 +522,22 @@ int ras_setup_device(const cpm_band* B, int S, int overlap, int k, double c, cud
     nloc[ls] = nl;
     ntl[ls] = nt;
   }
+  // segments start at multiples of 32 elements (256 B): the inner Krylov reduction
+  // pass then runs the register-direct kernel with 16-byte loads (vecops.cuh); the
+  // pad entries of a segment are zero in every inner vector (gidx -1, the apply never
+  // writes them) and add nothing to its dot products.  CPM_RAS_ALIGN=0: unpadded.
+  static const bool align = !(getenv("CPM_RAS_ALIGN") && *getenv("CPM_RAS_ALIGN") == '0');
+  const int64_t seg_align = align ? 32 : 1;
   R->off_h.assign(nsl + 1, 0);
   std::vector<int64_t> toff(nsl + 1, 0);
+  R->nmem = 0;
   for (int ls = 0; ls < nsl; ++ls) {
-    R->off_h[ls + 1] = R->off_h[ls] + nloc[ls];
+    R->off_h[ls + 1] = R->off_h[ls] + (nloc[ls] + seg_align - 1) / seg_align * seg_align;
     toff[ls + 1] = toff[ls] + ntl[ls];
+    R->nmem += nloc[ls];
   }
   R->ntot = R->off_h[nsl];
+  R->aligned = align ? 1 : 0;
   const int nTs = (int)toff[nsl];
   if (R->ntot >= INT32_MAX) return fail(CPM_ERR_LIMIT, "cpm_ras_setup: concatenated subdomains too large");
 
@@ -553,6 +564,7 @@ int ras_setup_device(const cpm_band* B, int S, int overlap, int k, double c, cud
   CPM_CUDA(cudaMalloc(&M.vb, sizeof(double) * kBrickCells * (size_t)std::max(nTs, 1)));
   CPM_CUDA(cudaMemsetAsync(M.vb, 0, sizeof(double) * kBrickCells * (size_t)std::max(nTs, 1), s));
   CPM_CUDA(cudaMalloc(&R->gidx, sizeof(int64_t) * std::max<int64_t>(R->ntot, 1)));
+  CPM_CUDA(cudaMemsetAsync(R->gidx, 0xff, sizeof(int64_t) * std::max<int64_t>(R->ntot, 1), s));  // pads: -1
 
   // phase B: per-subdomain structures
   DBuf tmap;
@@ -642,12 +654,13 @@ int ras_setup_device(const cpm_band* B, int S, int overlap, int k, double c, cud
       CPM_CUDA(cudaMemcpy(g.data(), R->gidx, sizeof(int64_t) * R->ntot, cudaMemcpyDeviceToHost));
     std::vector<int64_t>& H = R->halo_h;
     for (int64_t v : g)
-      if (v < own_lo || v >= own_lo + nown) H.push_back(v);
+      if (v >= 0 && (v < own_lo || v >= own_lo + nown)) H.push_back(v);
     std::sort(H.begin(), H.end());
     H.erase(std::unique(H.begin(), H.end()), H.end());
     for (int64_t& v : g)
-      v = (v >= own_lo && v < own_lo + nown) ? v - own_lo
-                                             : nown + (std::lower_bound(H.begin(), H.end(), v) - H.begin());
+      if (v >= 0)
+        v = (v >= own_lo && v < own_lo + nown) ? v - own_lo
+                                               : nown + (std::lower_bound(H.begin(), H.end(), v) - H.begin());
     if (R->ntot > 0)
       CPM_CUDA(cudaMemcpy(R->gidx, g.data(), sizeof(int64_t) * R->ntot, cudaMemcpyHostToDevice));
     R->nHalo = (int64_t)H.size();
@@ -677,9 +690,12 @@ int ras_setup_device(const cpm_band* B, int S, int overlap, int k, double c, cud
   R->ldv = (R->ntot + 63) / 64 * 64;
   CPM_CUDA(cudaMalloc(&R->V, sizeof(double) * (size_t)R->ldv * (k + 1)));
   CPM_CUDA(cudaMalloc(&R->W, sizeof(double) * (size_t)R->ldv));
+  CPM_CUDA(cudaMemsetAsync(R->W, 0, sizeof(double) * (size_t)R->ldv, s));  // pad entries stay 0
   int64_t maxn = 0;
   for (int ls = 0; ls < nsl; ++ls) maxn = std::max(maxn, nloc[ls]);
-  R->gps = (int)std::max<int64_t>(1, std::min<int64_t>((maxn + 255) / 256, std::max(1, kMaxBlocks / nsl / 2)));
+  // blocks per segment of the inner Krylov passes; CPM_RAS_GPS overrides (experiment)
+  const int gcap = getenv("CPM_RAS_GPS") ? std::max(1, atoi(getenv("CPM_RAS_GPS"))) : std::max(1, kMaxBlocks / nsl / 2);
+  R->gps = (int)std::max<int64_t>(1, std::min<int64_t>((maxn + 255) / 256, gcap));
   CPM_CUDA(cudaMalloc(&R->partial, sizeof(double) * (size_t)nsl * R->gps * (2 * (kMaxInner + 2) + 8)));
   CPM_CUDA(cudaMalloc(&R->st, sizeof(InnerState) * nsl));
   CPM_CUDA(cudaMemsetAsync(R->st, 0, sizeof(InnerState) * nsl, s));
@@ -703,7 +719,8 @@ int ras_apply_device(const cpm_ras* ras, const double* r, double* z, cudaStream_
   RasImpl* R = (RasImpl*)ras->impl;
   if (!r_halo) r_halo = R->hbuf;
   const int S = R->S, k = R->k;
-  const vec::Seg Sg{R->off, S, R->gps};
+  vec::Seg Sg{R->off, S, R->gps};
+  Sg.aligned = R->aligned;
   const int grid = S * R->gps;
   constexpr int lds = (int)(sizeof(InnerState) / sizeof(double));  // stride between segments' states
   InnerState* st = R->st;
@@ -797,7 +814,7 @@ int cpm_ras_get_info(const cpm_ras* ras, cpm_ras_info* info) {
   info->n_sub_local = R->S;
   info->rank = R->rank;
   info->nranks = R->nranks;
-  info->n_members = R->ntot;
+  info->n_members = R->nmem;
   info->n_owned = R->nOwned;
   info->n_halo = R->nHalo;
   info->n_send = R->nSend;

@@ -29,6 +29,7 @@ struct Seg {
   const int64_t* off;  // device, nseg + 1
   int nseg;
   int gps;             // blocks per segment
+  int aligned = 0;     // host hint: every off[s] is even (16-byte aligned segment starts)
 };
 
 __device__ __forceinline__ void cp_commit_v() { asm volatile("cp.async.commit_group;\n" ::); }
@@ -1126,9 +1127,10 @@ inline int launch_dcgs_dots_epi(const vec::Seg& S, int k, const double* V, int64
     const char* v = getenv("CPM_DOTS_DIRECT");
     return !v || *v != '0';
   }();
-  // the register-direct kernel for the single-segment (global) GMRES, whose columns are
-  // 16-byte aligned; the RAS segments start at arbitrary elements: the bulk-staged kernel
-  const bool direct = direct_env && S.nseg == 1;
+  // the register-direct kernel for the single-segment (global) GMRES and for aligned
+  // segments (the RAS inner solves pad each segment to 32 elements); unaligned
+  // segments: the bulk-staged kernel
+  const bool direct = direct_env && (S.nseg == 1 || S.aligned);
   // register-direct reduction pass: every owned column's loads of a tile issued
   // before its FMAs (UN = 0), columns per warp KW by k (fewer registers for small k)
   // CPM_DOTS_TMA=1: the TMA-staged variant (measured slower: 42.3 against 33.1 ms per
