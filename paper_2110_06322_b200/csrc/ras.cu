@@ -180,7 +180,7 @@ template <bool WRITE>
 __global__ void k_sub_runs(const TileHdr* sub, const TileHdr* tiles, const uint32_t* amask,
                            const int* bmap, const int* blo, const int* bdim, const uint64_t* bits,
                            int s, const int* pos, int64_t loff, const int64_t* rowbase,
-                           int64_t* rowcnt, const int64_t* runstart, uint64_t* runs) {
+                           int64_t* rowcnt, const int64_t* runstart, uint64_t* runs, int64_t zsrc) {
   const int q = blockIdx.x;
   const TileHdr T = sub[q];
   const int nrows = T.sy * T.sz;
@@ -203,8 +203,24 @@ __global__ void k_sub_runs(const TileHdr* sub, const TileHdr* tiles, const uint3
         while (lq < lxe) {
           const int cell = lq + 8 * ly + 64 * lz;
           const int a = mhas(m, cell) ? tiles[g].a0 + mrank(m, cell) : -1;
-          if (a < 0 || !((bits[a] >> s) & 1ull)) {
+          if (a < 0) {  // not in Sigma_A: no stencil reads it
             ++lq;
+            continue;
+          }
+          if (!((bits[a] >> s) & 1ull)) {
+            // Sigma_A cells outside the subdomain: a run from the zero source (src =
+            // zsrc reads the apply's zero buffer; with zsrc < 0 the box is cleared)
+            const int q0 = lq;
+            ++lq;
+            while (lq < lxe && mhas(m, lq + 8 * ly + 64 * lz) && !((bits[a + (lq - q0)] >> s) & 1ull)) ++lq;
+            if (zsrc >= 0) {
+              if (WRITE) {
+                const uint32_t dst =
+                    (uint32_t)((bx * 8 + q0 - T.ox) + T.pad[0] * (y - T.oy) + T.pad[1] * (z - T.oz));
+                runs[out + n] = pack_run((uint32_t)zsrc, dst, (uint32_t)(lq - q0));
+              }
+              ++n;
+            }
             continue;
           }
           const int q0 = lq;
@@ -439,11 +455,12 @@ struct RasImpl {
   int64_t ownLo = 0, nOwned = 0, nHalo = 0, nSend = 0;
   std::vector<int64_t> halo_h;                       // received global indices (sorted)
   double* hbuf = nullptr;                            // received values
+  double* zeros = nullptr;                           // the fill runs' zero source (16 doubles)
   int64_t* sendidx = nullptr;                        // owned local indices to send
   double* sendbuf = nullptr;
   std::vector<int64_t> sendCount, sendOff, recvCount, recvOff;
   ~RasImpl() {
-    void* ps[] = {off, gidx, lo, hi, xoff, V, W, partial, st, counters, hbuf, sendidx, sendbuf};
+    void* ps[] = {off, gidx, lo, hi, xoff, V, W, partial, st, counters, hbuf, sendidx, sendbuf, zeros};
     for (void* p : ps)
       if (p) cudaFree(p);
     void* mp[] = {mb.tiles, mb.runs, mb.vb, mb.acell};
@@ -552,7 +569,14 @@ int ras_setup_device(const cpm_band* B, int S, int overlap, int k, double c, cud
   M.nE = B->nE;
   M.nT = nTs;
   M.maxBox = B->maxBox;
-  M.zeroFill = true;
+  // cells of Sigma_A outside a subdomain are filled from a zero buffer (fill runs with
+  // source index ntot = srcSplit); CPM_RAS_ZRUNS=0: cleared boxes instead (zeroFill)
+  static const bool zruns = !(getenv("CPM_RAS_ZRUNS") && *getenv("CPM_RAS_ZRUNS") == '0');
+  const int64_t zsrc = zruns ? R->ntot : -1;
+  M.zeroFill = !zruns;
+  M.srcSplit = zruns ? (uint32_t)R->ntot : 0xffffffffu;
+  CPM_CUDA(cudaMalloc(&R->zeros, sizeof(double) * 16));
+  CPM_CUDA(cudaMemsetAsync(R->zeros, 0, sizeof(double) * 16, s));
   M.tx = B->tx;
   M.ty = B->ty;
   M.tz = B->tz;
@@ -615,7 +639,7 @@ int ras_setup_device(const cpm_band* B, int S, int overlap, int k, double c, cud
       k_sub_runs<false><<<nt, 128, 0, s>>>(M.tiles + to, B->tiles, B->amask, B->bmap, dblo.as<int>(),
                                            dbdim.as<int>(), bits, sd, pos.as<int>(), loff,
                                            rowbase.as<int64_t>(), rowcnt.as<int64_t>(), nullptr,
-                                           nullptr);
+                                           nullptr, zsrc);
       count_launch();
       CPM_TRY(scan(rowcnt.as<int64_t>(), runstart.as<int64_t>(), rows + 1, s));
       int64_t nr = 0;
@@ -624,7 +648,7 @@ int ras_setup_device(const cpm_band* B, int S, int overlap, int k, double c, cud
       k_sub_runs<true><<<nt, 128, 0, s>>>(M.tiles + to, B->tiles, B->amask, B->bmap, dblo.as<int>(),
                                           dbdim.as<int>(), bits, sd, pos.as<int>(), loff,
                                           rowbase.as<int64_t>(), rowcnt.as<int64_t>(),
-                                          runstart.as<int64_t>(), runbuf[ls].as<uint64_t>());
+                                          runstart.as<int64_t>(), runbuf[ls].as<uint64_t>(), zsrc);
       count_launch();
       int64_t roff = 0;
       for (int q = 0; q < ls; ++q) roff += nrun[q];
@@ -749,7 +773,8 @@ int ras_apply_device(const cpm_ras* ras, const double* r, double* z, cudaStream_
   // delayed CGS2 (krylov.cu): per inner step one apply, one reduction pass, one
   // update pass; step k only finalises the last Hessenberg column
   for (int j = 0; j <= k; ++j) {
-    if (j < k) CPM_TRY(apply_device(&R->mb, ras->c, R->V + (size_t)j * R->ldv, R->W, nullptr, 0, s));
+    if (j < k)
+      CPM_TRY(apply_device_split(&R->mb, ras->c, R->V + (size_t)j * R->ldv, R->zeros, R->W, nullptr, 0, s));
     {  // the block that completes segment s's reduction runs its step (epilogue)
       ProfScope ps(K_MDOT, s);
       CPM_TRY(launch_dcgs_dots_epi(Sg, j + 1, R->V, R->ldv, R->W, R->partial, 2 * (kMaxInner + 2) + 8,
