@@ -713,7 +713,7 @@ def run_partitioned(args):
                       "resid_true_rel": st.resid_true / st.bnorm,
                       "kind": f"partitioned GMRES(50) ({'host-transport' if host else 'NCCL'} allreduce)"},
             "setup_s": setup_s,
-            "roofline": {"kernel": "apply = halo exchange + k_extend_nt + k_laplace on each rank's sub-band",
+            "roofline": {"kernel": "apply = halo exchange + k_extend_nt + k_laplace_tma on each rank's sub-band",
                          "bound": "hbm", "achieved": achieved_per_gpu, "peak": peak, "unit": "GB/s",
                          "frac": achieved_per_gpu / peak, "traffic": None, "peak_source": peak_src,
                          "alg_bytes_per_apply_per_gpu": alg_bytes / ws, "apply_ms": mean_apply_s * 1e3,
