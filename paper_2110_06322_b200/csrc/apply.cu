@@ -897,6 +897,7 @@ static int laplace_tmaps(const cpm_band* b) {
 
 int laplace_tiles(const cpm_band* b, double c, const double* u, double* y, const double* scale, int lds,
                   cudaStream_t s, const int* skip) {
+  if (b->nT == 0) return CPM_OK;  // no tiles: no outputs (and no tensor map over an empty vb)
   const double ih2 = 1.0 / (b->h * b->h);
   const double diag = c + 6.0 * ih2;
   ProfScope ps(K_LAPLACE, s);
