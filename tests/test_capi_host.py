@@ -55,6 +55,9 @@ def test_argument_errors_without_gpu(lib):
     assert lib.cpm_build_band(ctypes.byref(s), 0.1, 3, 2.0, None, ctypes.byref(out)) == -1
     assert lib.cpm_apply(None, 1.0, None, None, None) == -1
     assert lib.cpm_solve(None, 1.0, None, None, 1e-10, 30, 10, None, None, None) == -1
+    assert lib.cpm_band_eval_order(None, None, None) == -1
+    assert lib.cpm_band_item_rounds(None, None) == -1
+    assert b"null" in lib.cpm_last_error()
     assert lib.cpm_profile_read(b"nope", None, None) == -1
     assert lib.cpm_profile_read(b"extend", None, None) == 0
 
