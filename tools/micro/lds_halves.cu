@@ -38,8 +38,9 @@ __global__ void __launch_bounds__(256) k(int iters, double* out, long long* cyc)
   double acc = 0.0;
   long long t0 = clock64();
   for (int it = 0; it < iters; ++it) {
+    const int sh = (it & 1) << 9;  // alternate two copies 512 doubles apart (same banks): no hoisting
 #pragma unroll
-    for (int q = 0; q < 64; ++q) acc += sm[ad[q]];
+    for (int q = 0; q < 64; ++q) acc += sm[(ad[q] + sh) & 4095];
   }
   long long t1 = clock64();
   if (acc == 12345.0) out[0] = acc;
