@@ -528,114 +528,84 @@ __device__ __forceinline__ void tma_4d(void* dst, const CUtensorMap* tm, int x, 
       : "memory");
 }
 
-template <int NT>
-__global__ void __launch_bounds__(128, NT == 1 ? 16 : 12)
-    k_laplace_tma(const TileHdr* __restrict__ tiles, int nT, const double* __restrict__ u,
-                  const uint16_t* __restrict__ acell, const double* __restrict__ vb, double* __restrict__ y,
-                  double diag, double ih2, const double* __restrict__ scale, int lds, const int* __restrict__ skip,
-                  int pfd, const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmY) {
-  // NT tiles per CTA (their copies all in flight before the first wait; NT = 1 is used)
-  __shared__ __align__(128) double own[NT][512];
-  __shared__ __align__(128) double fx[NT][2][128];  // [+x, -x] box 2 x 8 x 8: x + 2 y + 16 z
-  __shared__ __align__(128) double fy[NT][2][64];   // [+y, -y] box 8 x 1 x 8: x + 8 z
-  __shared__ __align__(128) double fz[NT][2][64];   // [+z, -z] layer: x + 8 y
-  __shared__ uint64_t bar[NT];
-  const int tid = threadIdx.x;
-  int tt[NT], a0[NT], a1[NT];
-  bool any = false;
-#pragma unroll
-  for (int j = 0; j < NT; ++j) {
-    tt[j] = nT - 1 - ((int)blockIdx.x * NT + j);  // reverse order: the extend's last tiles are in L2
-    a0[j] = a1[j] = 0;
-    if (tt[j] >= 0) {
-      a0[j] = tiles[tt[j]].a0;
-      a1[j] = tiles[tt[j]].a1;
-    }
-    any |= a0[j] < a1[j];
-  }
-  if (!any) return;
+__global__ void __launch_bounds__(128, 16) k_laplace_tma(const TileHdr* __restrict__ tiles, const double* __restrict__ u,
+                                                     const uint16_t* __restrict__ acell,
+                                                     const double* __restrict__ vb, double* __restrict__ y,
+                                                     double diag, double ih2, const double* __restrict__ scale,
+                                                     int lds, const int* __restrict__ skip, int pfd,
+                                                     const __grid_constant__ CUtensorMap tmX,
+                                                     const __grid_constant__ CUtensorMap tmY) {
+  __shared__ __align__(128) double own[512];
+  __shared__ __align__(128) double fx[2][128];  // [+x, -x] box 2 x 8 x 8: x + 2 y + 16 z
+  __shared__ __align__(128) double fy[2][64];   // [+y, -y] box 8 x 1 x 8: x + 8 z
+  __shared__ __align__(128) double fz[2][64];   // [+z, -z] layer: x + 8 y
+  __shared__ uint64_t bar;
+  const int t = (int)gridDim.x - 1 - (int)blockIdx.x, tid = threadIdx.x;
+  const TileHdr* T = tiles + t;
+  const int a0 = T->a0, a1 = T->a1;
+  if (a0 == a1) return;
   if (tid == 0) {
-#pragma unroll
-    for (int j = 0; j < NT; ++j)
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(sm32(&bar[j])) : "memory");
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(sm32(&bar)) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
-  if (tid == 32) {  // a later CTA's tiles into L2
-#pragma unroll
-    for (int j = 0; j < NT; ++j) {
-      const int tf = tt[j] - pfd;
-      if (tf < 0) continue;
-      const TileHdr* F = tiles + tf;
-      const int f0 = F->a0, f1 = F->a1;
-      prefetch_l2_bytes(acell + f0, (size_t)(f1 - f0) * 2);
-      prefetch_l2_bytes(u + f0, (size_t)(f1 - f0) * 8);
-      prefetch_l2_bytes(vb + (size_t)tf * kBrickCells, kBrickCells * 8);
-    }
+  if (tid == 32 && t - pfd >= 0) {  // a later CTA's tile into L2
+    const TileHdr* F = tiles + t - pfd;
+    const int f0 = F->a0, f1 = F->a1;
+    prefetch_l2_bytes(acell + f0, (size_t)(f1 - f0) * 2);
+    prefetch_l2_bytes(u + f0, (size_t)(f1 - f0) * 8);
+    prefetch_l2_bytes(vb + (size_t)(t - pfd) * kBrickCells, kBrickCells * 8);
   }
-  int ac[NT][4];
-  double au[NT][4];
+  int ac[4];
+  double au[4];
 #pragma unroll
-  for (int j = 0; j < NT; ++j)
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int a = a0[j] + tid + k * 128;
-      if (a < a1[j]) ac[j][k] = __ldg(acell + a);
-    }
-  __syncthreads();  // mbarriers initialised
+  for (int k = 0; k < 4; ++k) {
+    const int a = a0 + tid + k * 128;
+    if (a < a1) ac[k] = __ldg(acell + a);
+  }
+  __syncthreads();  // mbarrier initialised
   pdl_wait();       // the extend (E u) and the producer of u have completed
   if (skip && *skip) return;
   if (tid == 0) {
+    int nb[6];
+    unsigned bytes = kBrickCells * 8;
 #pragma unroll
-    for (int j = 0; j < NT; ++j) {
-      if (a0[j] == a1[j]) continue;
-      const TileHdr* T = tiles + tt[j];
-      int nb[6];
-      unsigned bytes = kBrickCells * 8;
-#pragma unroll
-      for (int f = 0; f < 6; ++f) {
-        nb[f] = T->nbr[f];
-        if (nb[f] >= 0) bytes += f < 2 ? 1024u : 512u;
-      }
-      uint64_t* b = &bar[j];
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(sm32(b)), "r"(bytes) : "memory");
-      tma_bulk(own[j], vb + (size_t)tt[j] * kBrickCells, kBrickCells * 8, b);
-      if (nb[0] >= 0) tma_4d(fx[j][0], &tmX, 0, 0, 0, nb[0], b);  // +x neighbour: its x = 0 layer
-      if (nb[1] >= 0) tma_4d(fx[j][1], &tmX, 6, 0, 0, nb[1], b);  // -x neighbour: x = 7 (box x = 6, 7)
-      if (nb[2] >= 0) tma_4d(fy[j][0], &tmY, 0, 0, 0, nb[2], b);
-      if (nb[3] >= 0) tma_4d(fy[j][1], &tmY, 0, 7, 0, nb[3], b);
-      if (nb[4] >= 0) tma_bulk(fz[j][0], vb + (size_t)nb[4] * kBrickCells, 512, b);
-      if (nb[5] >= 0) tma_bulk(fz[j][1], vb + (size_t)nb[5] * kBrickCells + 448, 512, b);
+    for (int f = 0; f < 6; ++f) {
+      nb[f] = T->nbr[f];
+      if (nb[f] >= 0) bytes += f < 2 ? 1024u : 512u;
     }
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(sm32(&bar)), "r"(bytes)
+                 : "memory");
+    tma_bulk(own, vb + (size_t)t * kBrickCells, kBrickCells * 8, &bar);
+    if (nb[0] >= 0) tma_4d(fx[0], &tmX, 0, 0, 0, nb[0], &bar);  // +x neighbour: its x = 0 layer
+    if (nb[1] >= 0) tma_4d(fx[1], &tmX, 6, 0, 0, nb[1], &bar);  // -x neighbour: x = 7 (box x = 6, 7)
+    if (nb[2] >= 0) tma_4d(fy[0], &tmY, 0, 0, 0, nb[2], &bar);
+    if (nb[3] >= 0) tma_4d(fy[1], &tmY, 0, 7, 0, nb[3], &bar);
+    if (nb[4] >= 0) tma_bulk(fz[0], vb + (size_t)nb[4] * kBrickCells, 512, &bar);
+    if (nb[5] >= 0) tma_bulk(fz[1], vb + (size_t)nb[5] * kBrickCells + 448, 512, &bar);
   }
 #pragma unroll
-  for (int j = 0; j < NT; ++j)
+  for (int k = 0; k < 4; ++k) {
+    const int a = a0 + tid + k * 128;
+    if (a < a1) au[k] = __ldg(u + a);
+  }
+  const double s = scale ? __ldg(scale + (size_t)T->pad[2] * lds) : 1.0;
+  asm volatile(
+      "{\n .reg .pred p;\n WAITL_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n"
+      " @!p bra WAITL_%=;\n}\n" ::"r"(sm32(&bar))
+      : "memory");
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int a = a0[j] + tid + k * 128;
-      if (a < a1[j]) au[j][k] = __ldg(u + a);
-    }
-#pragma unroll
-  for (int j = 0; j < NT; ++j) {
-    if (a0[j] == a1[j]) continue;
-    const double s = scale ? __ldg(scale + (size_t)tiles[tt[j]].pad[2] * lds) : 1.0;
-    asm volatile(
-        "{\n .reg .pred p;\n WAITL_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n"
-        " @!p bra WAITL_%=;\n}\n" ::"r"(sm32(&bar[j]))
-        : "memory");
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int a = a0[j] + tid + k * 128;
-      if (a < a1[j]) {
-        const int c = ac[j][k], x = c & 7, yy = (c >> 3) & 7, z = c >> 6;
-        const double xp = x < 7 ? own[j][c + 1] : fx[j][0][2 * yy + 16 * z];
-        const double xm = x > 0 ? own[j][c - 1] : fx[j][1][1 + 2 * yy + 16 * z];
-        const double yp = yy < 7 ? own[j][c + 8] : fy[j][0][x + 8 * z];
-        const double ym = yy > 0 ? own[j][c - 8] : fy[j][1][x + 8 * z];
-        const double zp = z < 7 ? own[j][c + 64] : fz[j][0][x + 8 * yy];
-        const double zm = z > 0 ? own[j][c - 64] : fz[j][1][x + 8 * yy];
-        const double sum = xp + xm + yp + ym + zp + zm;
-        y[a] = s * (diag * au[j][k] - ih2 * sum);
-      }
+  for (int k = 0; k < 4; ++k) {
+    const int a = a0 + tid + k * 128;
+    if (a < a1) {
+      const int c = ac[k], x = c & 7, yy = (c >> 3) & 7, z = c >> 6;
+      const double xp = x < 7 ? own[c + 1] : fx[0][2 * yy + 16 * z];
+      const double xm = x > 0 ? own[c - 1] : fx[1][1 + 2 * yy + 16 * z];
+      const double yp = yy < 7 ? own[c + 8] : fy[0][x + 8 * z];
+      const double ym = yy > 0 ? own[c - 8] : fy[1][x + 8 * z];
+      const double zp = z < 7 ? own[c + 64] : fz[0][x + 8 * yy];
+      const double zm = z > 0 ? own[c - 64] : fz[1][x + 8 * yy];
+      const double sum = xp + xm + yp + ym + zp + zm;
+      y[a] = s * (diag * au[k] - ih2 * sum);
     }
   }
 }
@@ -911,9 +881,9 @@ int laplace_tiles(const cpm_band* b, double c, const double* u, double* y, const
     std::memcpy(&my, b->tmY, sizeof(CUtensorMap));
     // one tile per CTA (two tiles per CTA, both tiles' copies in flight before the
     // first wait: 45.5 us against 35.5, measured)
-    CPM_CUDA(launch_pdl_l2(vb_window(b), k_laplace_tma<1>, dim3((unsigned)b->nT), dim3(128), 0, s, b->tiles,
-                             b->nT, u, (const uint16_t*)b->acell, (const double*)b->vb, y, diag, ih2, scale, lds,
-                             skip, pfd2, mx, my));
+    CPM_CUDA(launch_pdl_l2(vb_window(b), k_laplace_tma, dim3((unsigned)b->nT), dim3(128), 0, s, b->tiles, u,
+                           (const uint16_t*)b->acell, (const double*)b->vb, y, diag, ih2, scale, lds, skip, pfd2,
+                           mx, my));
     count_launch();
     CPM_CUDA(cudaGetLastError());
     return CPM_OK;
