@@ -160,9 +160,11 @@ __global__ void __launch_bounds__(kNtThreads, MINB)
   uint64_t* desc = (uint64_t*)(box + boxCells);
   const int t = tbase + (int)blockIdx.x, tid = threadIdx.x;  // tiles [tbase, tend)
   const TileHdr* T = tiles + t;
-  const int e0 = T->e0, ne = T->e1 - e0, r0 = T->r0, r1 = T->r1;
-  const int np2 = 2 * T->np, nd = T->pad2, nslot = ne + nd;
-  const int sx = T->pad[0], sxy = T->pad[1];
+  const int4 h0 = __ldg((const int4*)T), h1 = __ldg((const int4*)T + 1);  // e0 e1 a0 a1 | r0 r1 np pad2
+  const int2 h2 = __ldg((const int2*)T->pad);                                // row, plane stride
+  const int e0 = h0.x, ne = h0.y - e0, r0 = h1.x, r1 = h1.y;
+  const int np2 = 2 * h1.z, nd = h1.w, nslot = ne + nd;
+  const int sx = h2.x, sxy = h2.y;
   const uint64_t pfirst = policy_evict_first(), plast = policy_evict_last();
   // the first kNtPre slots of this thread are requested before the box is staged
   double nt[kNtPre][3];
@@ -542,7 +544,8 @@ __global__ void __launch_bounds__(128, 16) k_laplace_tma(const TileHdr* __restri
   __shared__ uint64_t bar;
   const int t = (int)gridDim.x - 1 - (int)blockIdx.x, tid = threadIdx.x;
   const TileHdr* T = tiles + t;
-  const int a0 = T->a0, a1 = T->a1;
+  const int4 h0 = __ldg((const int4*)T);  // e0 e1 a0 a1
+  const int a0 = h0.z, a1 = h0.w;
   if (a0 == a1) return;
   if (tid == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(sm32(&bar)) : "memory");
