@@ -16,7 +16,8 @@ from dataclasses import dataclass
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libcpm.so")
+# CPM_LIB_PATH: another in-tree build of the same library (kernel A/B timing only)
+LIB_PATH = os.environ.get("CPM_LIB_PATH") or os.path.join(_HERE, "_lib", "libcpm.so")
 
 SPHERE = 1
 TORUS = 2
