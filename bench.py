@@ -416,6 +416,28 @@ def run_mine(args):
         torch.cuda.synchronize()
         e2e_sync_s = time.perf_counter() - t_e
 
+    # the e2e roof: the same bytes per apply (u in, y out) copied with nothing else,
+    # H2D and D2H concurrently on two streams (the host link's rate for this traffic)
+    link_value = None
+    try:
+        d_in = torch.empty(nA, dtype=torch.float64, device=dev)
+        d_out = torch.empty(nA, dtype=torch.float64, device=dev)
+        s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
+        reps = 20
+        for _ in range(2):
+            torch.cuda.synchronize()
+            t_l = time.perf_counter()
+            for _ in range(reps):
+                with torch.cuda.stream(s_in):
+                    d_in.copy_(u_host, non_blocking=True)
+                with torch.cuda.stream(s_out):
+                    y_host.copy_(d_out, non_blocking=True)
+            torch.cuda.synchronize()
+            link_value = nA * reps / (time.perf_counter() - t_l)
+        del d_in, d_out
+    except Exception:
+        link_value = None
+
     solve_med_ms = float(np.median(solve_ms))
     n_applies = CFG["applies"] * args.steps
     value = nA * n_applies / (apply_ms / 1e3)
@@ -481,7 +503,12 @@ def run_mine(args):
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 8 * nA * CFG["applies"],
                     "d2h_bytes_per_step": 8 * nA * CFG["applies"],
                     "api": "cpm_apply_async on pinned host buffers (+ cpm_apply_sync), 100 applies per step",
-                    "sync_cpm_apply_value": (nA * CFG["applies"] / e2e_sync_s) if e2e_sync_s else None},
+                    "sync_cpm_apply_value": (nA * CFG["applies"] / e2e_sync_s) if e2e_sync_s else None,
+                    "link_bound_value": link_value,
+                    "link_frac": (e2e_value / link_value) if link_value else None,
+                    "link_note": "link_bound_value: the same 8 B in + 8 B out per active node copied alone "
+                                 "(pinned, H2D and D2H concurrent on two streams), the host link's roof "
+                                 "for e2e"},
             "config4_rd": rd,
             "config2_solve": c2,
             "config3_solve": c3,
