@@ -122,6 +122,17 @@ def _traffic():
         return None
 
 
+def _l1tex_events():
+    """l1tex data-stage events (shared wavefronts + global tag requests) of one config-1
+    extend launch, from the committed ncu capture (profiles/r02_ncu_v3.txt)."""
+    p = os.path.join(ROOT, "profiles", "r02_l1tex_events.json")
+    try:
+        d = json.load(open(p))
+        return float(d["shared_wavefronts"]) + float(d["global_tag_requests"])
+    except Exception:
+        return None
+
+
 def _dist():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -449,6 +460,19 @@ def run_mine(args):
     mean_apply_s = apply_ms / 1e3 / (CFG["applies"] * args.steps)
     achieved = alg_bytes / mean_apply_s / 1e9
     traffic = _traffic()
+    # what limits the extend (not HBM): its l1tex data stage, one shared wavefront or one
+    # global tag request per clock per SM; events from the ncu capture, the clock and the
+    # time measured in this run
+    l1ev = _l1tex_events()
+    ext_s = ext_ms / max(ext_n, 1) / 1e3
+    sm_hz = (clk.get("sm_mhz") or 0.0) * 1e6
+    limiter = None
+    if l1ev and ext_s > 0 and sm_hz > 0:
+        per_clk = l1ev / (ext_s * 148 * sm_hz)
+        limiter = {"kernel": "k_extend_nt", "bound": "l1tex data stage (shared-memory wavefronts + global tag "
+                   "requests)", "events_per_launch": l1ev, "achieved": per_clk, "peak": 1.0,
+                   "unit": "events/clk/SM", "frac": per_clk, "sm_mhz": clk.get("sm_mhz"),
+                   "source": "profiles/r02_l1tex_events.json (ncu), time and clock of this run"}
     # Krylov passes of the solve (delayed CGS2): per Arnoldi step j one reduction
     # pass (reads V_0..V_j and z: (j + 2) * 8 n bytes) and one update pass (reads the
     # same, writes q_j and u_{j+1}: (j + 4) * 8 n bytes); steps j = 0 .. per cycle
@@ -481,6 +505,8 @@ def run_mine(args):
             "roofline": {"kernel": "apply = k_extend_nt + k_laplace_tma (one apply, the metric's unit)",
                          "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                         "frac_of_nominal_8tbs": achieved / 8000.0,   # north_star's denominator
+                         "limiter": limiter,
                          "alg_bytes_per_apply": alg_bytes,
                          "apply_ms": mean_apply_s * 1e3,
                          "extend_ms": ext_ms / max(ext_n, 1), "laplace_ms": lap_ms / max(lap_n, 1),
