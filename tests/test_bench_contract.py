@@ -47,6 +47,9 @@ def test_gpu_arm_json_line():
     r = d["roofline"]
     assert r["bound"] == "hbm" and r["unit"] == "GB/s" and 0 < r["frac"] < 1
     assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-9
+    assert abs(r["frac_of_nominal_8tbs"] - r["achieved"] / 8000.0) < 1e-9
+    lim = r["limiter"]          # the extend's l1tex data stage: events / (time x SMs x clock) <= 1
+    assert lim["kernel"] == "k_extend_nt" and lim["peak"] == 1.0 and 0.3 < lim["frac"] <= 1.0
     assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["value"] > 0
     assert d["gpu_launches"] > 0
     assert d["solve"]["converged"] and d["solve"]["resid_true_rel"] < 1e-9
