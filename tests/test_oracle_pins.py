@@ -372,6 +372,13 @@ def test_order_key_hand_values():
     # brick -1 in x: 2^16 - 1 = 0xFFFF interleaved -> bits 0,3,...,45
     m = sum(1 << (3 * b) for b in range(16)) | (1 << 49) | (1 << 50)
     assert k[5] == m * 512 + 7
+    # the axes of the brick Morton key (reading R8: x bits lowest, then y, then z): bit b
+    # of the brick's x, y, z index sits at key bit 3b, 3b + 1, 3b + 2
+    k2 = band_order_key(np.array([[0, 8, 0], [0, 0, 8], [0, 16, 0], [0, 0, 16], [16, 8, 24]]))
+    assert k2[0] == (base | 2) * 512 and k2[1] == (base | 4) * 512
+    assert k2[2] == (base | (1 << 4)) * 512 and k2[3] == (base | (1 << 5)) * 512
+    # bricks (2, 1, 3): x bit 1 -> key bit 3; y bit 0 -> 1; z bits 0, 1 -> 2, 5
+    assert k2[4] == (base | (1 << 3) | (1 << 1) | (1 << 2) | (1 << 5)) * 512
 
 
 def test_partition_and_overlap_invariants():
