@@ -19,7 +19,7 @@ from oracle.interp import OFFS, extension_matrix, extension_rows, lagrange_weigh
 from oracle.krylov import arnoldi_fixed, gmres
 from oracle.operator import apply_rows, laplace_beltrami_matrix, laplacian_matrix, shifted_operator
 from oracle.order import band_order_key, slab_bounds
-from oracle.problems import exact_sph, rhs_sph
+from oracle.problems import exact_sph, rhs_noisy_sph, rhs_sph, rhs_torus, torus_angles
 from oracle.ras import RAS, disjoint_subdomains, grow_overlap
 from oracle.sph import real_sph
 from oracle.surfaces import Plane, Sphere, Torus
@@ -505,3 +505,89 @@ def test_schnakenberg_initial_state_recipe():
     u, v = initial_state(b, p)
     assert np.all(np.abs(u - 1.0) <= 1e-2) and np.all(np.abs(v - 0.9) <= 1e-2)
     assert abs(np.corrcoef(u, v)[0, 1]) < 0.1
+    # the state the noise is added to is the kinetics' fixed point (configs[4]: u = a + b,
+    # v = b/(a+b)^2); with the default a + b = 1 the square cannot be seen, so a + b = 1.25
+    q = SchnakenbergParams(a=0.25, b=1.0)
+    u, v = initial_state(b, q)
+    ru, rv = reaction(np.array([u.mean()]), np.array([v.mean()]), q)
+    assert abs(ru[0]) < 5e-3 * q.gamma and abs(rv[0]) < 5e-3 * q.gamma
+    assert abs(v.mean() - 0.64) < 1e-3
+
+
+# ---------------------------------------------------------------- conventions found unpinned by tools/oracle_mutations.py
+def test_real_sph_closed_forms_low_degree():
+    """Reading R9 (real, orthonormal, +m = cos branch, -m = sin branch, no Condon-Shortley
+    phase): the textbook Cartesian forms Y_1^1 = sqrt(3/4pi) x, Y_1^-1 = sqrt(3/4pi) y,
+    Y_1^0 = sqrt(3/4pi) z, Y_2^2 = (1/4) sqrt(15/pi) (x^2 - y^2), Y_2^-2 = (1/2) sqrt(15/pi) x y,
+    Y_2^1 = (1/2) sqrt(15/pi) x z on the unit sphere."""
+    rng = np.random.default_rng(5)
+    p = rng.normal(size=(200, 3))
+    p /= np.linalg.norm(p, axis=1)[:, None]
+    x, y, z = p.T
+    c1 = math.sqrt(3.0 / (4.0 * math.pi))
+    c2 = math.sqrt(15.0 / math.pi)
+    for (l, m), want in {(1, 1): c1 * x, (1, -1): c1 * y, (1, 0): c1 * z, (2, 2): 0.25 * c2 * (x * x - y * y),
+                         (2, -2): 0.5 * c2 * x * y, (2, 1): 0.5 * c2 * x * z}.items():
+        assert np.allclose(real_sph(l, m, 3.0 * p), want, atol=1e-13), (l, m)
+
+
+def test_torus_angles_invert_the_parametrisation():
+    """Reading R10: ph = toroidal angle about the z axis, th = poloidal angle about the core
+    circle.  Points built from ((R + r cos th) cos ph, (R + r cos th) sin ph, r sin th) give
+    their angles back."""
+    R, r = 1.0, 0.4
+    th, ph = np.meshgrid(np.linspace(-3.0, 3.0, 13), np.linspace(-3.1, 3.1, 17), indexing="ij")
+    th, ph = th.ravel(), ph.ravel()
+    rho = R + r * np.cos(th)
+    pts = np.stack([rho * np.cos(ph), rho * np.sin(ph), r * np.sin(th)], axis=1)
+    th2, ph2 = torus_angles(pts, R)
+    assert np.allclose(th2, th, atol=1e-12) and np.allclose(ph2, ph, atol=1e-12)
+
+
+def test_rhs_torus_symmetries_and_zero_crossings():
+    """configs[2]: f = cos(3 th) sin(2 ph) x modulation, modulation in [0.5, 1.5] (> 0), so
+    the sign pattern of f is that of cos(3 th) sin(2 ph): odd under the quarter turn about z
+    (ph -> ph + pi/2), even under z -> -z (th -> -th); 4 sign changes once around the outer
+    equator (th = 0) and 6 once around the poloidal circle in the half plane x = y > 0."""
+    h = 0.1
+    b = Band(Torus(1.0, 0.4), h)
+    ijk = b.active
+    f = rhs_torus(b, 1, ijk)
+    big = np.abs(f) > 0.05
+    rot = np.stack([-ijk[:, 1], ijk[:, 0], ijk[:, 2]], axis=1)          # quarter turn about z
+    refl = ijk * np.array([1, 1, -1])
+    assert np.all(np.sign(rhs_torus(b, 1, rot)[big]) == -np.sign(f[big]))
+    assert np.all(np.sign(rhs_torus(b, 1, refl)[big]) == np.sign(f[big]))
+    assert 0.9 < np.abs(f).max() < 1.5
+
+    def crossings(vals):
+        sg = np.sign(vals[np.abs(vals) > 1e-6])
+        return int(np.sum(sg != np.roll(sg, 1)))
+
+    # outer equator: nodes of the plane z = 0 beyond the core circle by more than r/2
+    rho = h * np.hypot(ijk[:, 0], ijk[:, 1])
+    eq = (ijk[:, 2] == 0) & (rho > 1.0 + 0.2)
+    order = np.argsort(np.arctan2(ijk[eq, 1], ijk[eq, 0]))
+    assert crossings(f[eq][order]) == 4
+    # poloidal circle: nodes of the half plane x = y > 0, ordered by their angle about the core circle
+    pc = (ijk[:, 0] == ijk[:, 1]) & (ijk[:, 0] > 0)
+    ang = np.arctan2(h * ijk[pc, 2], rho[pc] - 1.0)
+    assert crossings(f[pc][np.argsort(ang)]) == 6
+
+
+def test_rhs_noisy_sph_noise_level():
+    """configs[3]: f = Y_10^5(cp(x)) + 1e-3 N(0,1): what is left after subtracting the
+    harmonic has sample standard deviation 1e-3 (n ~ 1e4: +-1.5 %) and zero mean."""
+    b = Band(Sphere(1.0), 0.1)
+    d = rhs_noisy_sph(b, 10, 5, 2) - exact_sph(b, 10, 5)
+    assert abs(d.std() / 1e-3 - 1.0) < 0.05 and abs(d.mean()) < 5e-5
+
+
+def test_ras_subdomains_are_band_order_slabs():
+    """Reading R8 (north_star 4: Morton-slab subdomains): subdomain s is the s-th contiguous
+    range of the band order, so every band-order key of S~_s is below every key of S~_{s+1}."""
+    b = Band(Sphere(1.0), 0.15)
+    key = band_order_key(b.active)
+    dis = disjoint_subdomains(b, 5)
+    for s in range(4):
+        assert key[dis[s]].max() < key[dis[s + 1]].min()

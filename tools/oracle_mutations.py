@@ -75,6 +75,42 @@ MUTATIONS = {
                         "return (c + l * l) * real_sph(l, m, cp_of(band, ijk))")],
     # restarted GMRES: the correction of a cycle added with the wrong sign
     "gmres_modified_gs": [("oracle/krylov.py", "w = w - H[i, j] * V[i]", "w = w + H[i, j] * V[i]")],
+    # torus closest point with the major radius in place of the minor one
+    "torus_cp_radius": [("oracle/surfaces.py", "cp[:, 2] = (self.r * dz) / dn", "cp[:, 2] = (self.R * dz) / dn")],
+    # torus distance to the core circle instead of the surface
+    "torus_dist": [("oracle/surfaces.py", "dist = np.abs(dn - self.r)\n        bad = (rho == 0.0) | (dn == 0.0)",
+                    "dist = np.abs(dn)\n        bad = (rho == 0.0) | (dn == 0.0)")],
+    # interpolation nodes (-1, 0, 1, 2) shifted to (0, 1, 2, 3)
+    "lagrange_nodes": [("oracle/interp.py", "TAU = np.array([-1.0, 0.0, 1.0, 2.0])", "TAU = np.array([0.0, 1.0, 2.0, 3.0])")],
+    # 7-point Laplacian with a 5 on the diagonal
+    "laplacian_diagonal": [("oracle/operator.py", "vals = [np.full(nA, -6.0 / h2)]", "vals = [np.full(nA, -5.0 / h2)]")],
+    # real spherical harmonics without the sqrt(2) of m != 0
+    "sph_normalisation": [("oracle/sph.py", "return math.sqrt(2.0) * K * P * np.cos(am * ph)", "return K * P * np.cos(am * ph)")],
+    # cos and sin branches of +m / -m swapped
+    "sph_branches": [("oracle/sph.py", "if m > 0:\n        return math.sqrt(2.0) * K * P * np.cos(am * ph)",
+                      "if m < 0:\n        return math.sqrt(2.0) * K * P * np.cos(am * ph)")],
+    # config-2 rhs with the poloidal and toroidal angles exchanged
+    "torus_rhs_angles": [("oracle/problems.py", "return np.cos(3.0 * th) * np.sin(2.0 * ph) * mod",
+                          "return np.cos(3.0 * ph) * np.sin(2.0 * th) * mod")],
+    # poloidal angle about the z axis instead of the core circle
+    "torus_theta": [("oracle/problems.py", "th = np.arctan2(cp[:, 2], rho - R)", "th = np.arctan2(cp[:, 2], rho)")],
+    # config-3 rhs noise amplitude
+    "noise_amplitude": [("oracle/problems.py", "+ 1e-3 * seeded_inputs.normal(seed, ijk)", "+ 1e-2 * seeded_inputs.normal(seed, ijk)")],
+    # GMRES: tolerance relative to the initial residual of each cycle instead of ||b||
+    "gmres_target": [("oracle/krylov.py", "        beta = float(np.linalg.norm(r))\n        if beta <= target:",
+                      "        beta = float(np.linalg.norm(r))\n        target = rtol * beta\n        if beta <= target:")],
+    # GMRES: restart from zero instead of the current iterate
+    "gmres_restart_update": [("oracle/krylov.py", "        x = x + Z[:k].T @ y", "        x = Z[:k].T @ y")],
+    # RAS: restriction of the residual to the disjoint part only (no overlap data)
+    "ras_keep_shift": [("oracle/ras.py", "self.keep = [np.searchsorted(o, d) for o, d in zip(self.over, self.disjoint)]",
+                        "self.keep = [np.minimum(np.searchsorted(o, d) + 1, len(o) - 1) for o, d in zip(self.over, self.disjoint)]")],
+    # RAS subdomains as slabs of the lattice-key order instead of the band (Morton) order
+    "ras_slab_order": [("oracle/ras.py", "perm = band_order(band.active)", "perm = np.arange(band.nA)")],
+    # Schnakenberg initial state: v = b / (a + b) instead of b / (a + b)^2
+    "initial_state_v": [("oracle/reaction.py", "vs = p.b / (p.a + p.b) ** 2", "vs = p.b / (p.a + p.b)")],
+    # slab bounds rounded up
+    "slab_bounds_ceil": [("oracle/order.py", "return [(s * n) // S for s in range(S + 1)]",
+                          "return [-((-s * n) // S) for s in range(S + 1)]")],
 }
 
 
@@ -90,6 +126,14 @@ HINTS = {
     "reaction_sign": "schnakenberg_constant_state", "imex_dt": "schnakenberg_constant_state",
     "imex_mu_swapped": "schnakenberg_constant_state", "rhs_eigenvalue": "manufactured_solution_second_order",
     "gmres_modified_gs": "gmres_identity_one_iteration",
+    "torus_cp_radius": "torus_cp_matches_brute_force", "torus_dist": "band_matches_pure_python",
+    "lagrange_nodes": "lagrange_weights_golden", "laplacian_diagonal": "delta_h_exact_on_quadratics",
+    "sph_normalisation": "real_sph_orthonormal", "sph_branches": "real_sph_closed_forms",
+    "torus_rhs_angles": "rhs_torus_symmetries", "torus_theta": "torus_angles_invert",
+    "noise_amplitude": "rhs_noisy_sph_noise_level", "gmres_target": "gmres_dense_random_vs_lu",
+    "gmres_restart_update": "gmres_dense_random_vs_lu", "ras_keep_shift": "ras_single_subdomain_exact",
+    "ras_slab_order": "ras_subdomains_are_band_order_slabs", "initial_state_v": "initial_state_recipe",
+    "slab_bounds_ceil": "partition_and_overlap_invariants",
 }
 
 
