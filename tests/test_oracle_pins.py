@@ -61,6 +61,11 @@ def test_sphere_cp_closed_form():
     assert np.allclose(np.linalg.norm(x - cp, axis=1), d, atol=1e-15)
     cp2, d2 = Sphere(1.0).cp(cp)                     # idempotence
     assert np.all(d2 < 1e-15)
+    # radius R != 1 (cp = R x/|x|, PAPER.md:56-60 with the sphere's closed form)
+    cp3, d3 = Sphere(2.5).cp(x)
+    assert np.allclose(cp3[0], [2.5, 0, 0]) and d3[0] == 0.5
+    assert np.allclose(cp3[1], [1.5, -2.0, 0]) and abs(d3[1] - 2.0) < 1e-15
+    assert np.allclose(np.linalg.norm(x - cp3, axis=1), d3, atol=1e-15)
 
 
 def _torus_pt(p):

@@ -111,6 +111,43 @@ MUTATIONS = {
     # slab bounds rounded up
     "slab_bounds_ceil": [("oracle/order.py", "return [(s * n) // S for s in range(S + 1)]",
                           "return [-((-s * n) // S) for s in range(S + 1)]")],
+    # sphere closest point without the radius
+    "sphere_radius": [("oracle/surfaces.py", "cp = (self.R * x) / r[:, None]", "cp = x / r[:, None]")],
+    # fractional offset measured from the wrong lattice node (t = ceil - s)
+    "stencil_offset": [("oracle/interp.py", "t = s - fl", "t = 1.0 - (s - fl)")],
+    # barycentric weights without their alternating sign
+    "barycentric_sign": [("oracle/interp.py", "beta[j] = 1.0 / prod", "beta[j] = abs(1.0 / prod)")],
+    # row formula: five of the six neighbours
+    "apply_rows_neighbours": [("oracle/operator.py", "    for off in NEIGHBORS6:\n        nb = nb + Eu_at(rows_ijk + off[None, :])",
+                               "    for off in NEIGHBORS6[:5]:\n        nb = nb + Eu_at(rows_ijk + off[None, :])")],
+    # row formula: u instead of E u at the neighbours (no extension before the stencil)
+    "apply_rows_no_extension": [("oracle/operator.py", "        nb = nb + Eu_at(rows_ijk + off[None, :])",
+                                 "        nb = nb + u_of_ijk(rows_ijk + off[None, :])")],
+    # assembled operator: Delta_h applied to u, not to E u
+    "laplacian_without_E": [("oracle/operator.py",
+                             'return (-d2 * sp.identity(nA, format="csr") + (Dh + d2 * P) @ E).tocsr()',
+                             'return (-d2 * sp.identity(nA, format="csr") + (Dh[:, :nA] + d2 * P[:, :nA])).tocsr()')],
+    # ghost columns indexed without the nA offset
+    "ghost_index_offset": [("oracle/band.py", "return np.where(ia >= 0, ia, np.where(ig >= 0, ig + self.nA, -1))",
+                            "return np.where(ia >= 0, ia, np.where(ig >= 0, ig, -1))")],
+    # GMRES: an iteration counted per Gram-Schmidt column as well
+    "gmres_its_count": [("oracle/krylov.py", "            w = A(Z[j])\n            its += 1", "            w = A(Z[j])\n            its += 2")],
+    # GMRES: back substitution over the wrong triangle
+    "gmres_back_substitution": [("oracle/krylov.py", "y[i] = (g[i] - np.dot(H[i, i + 1:k], y[i + 1:k])) / H[i, i]",
+                                 "y[i] = (g[i] - np.dot(H[i + 1:k, i], y[i + 1:k])) / H[i, i]")],
+    # FGMRES: update with the Krylov basis V instead of the preconditioned vectors Z
+    "fgmres_update_basis": [("oracle/krylov.py", "        x = x + Z[:k].T @ y", "        x = x + V[:k].T @ y")],
+    # overlap grown through all 26 neighbours (reading R7: 6-neighbour layers)
+    "overlap_26": [("oracle/ras.py", "    for _ in range(layers):\n        grow = inside.copy()",
+                    "    for _ in range(2 * layers):\n        grow = inside.copy()")],
+    # IMEX: (c + Delta) instead of (c - Delta)
+    "imex_operator_sign": [("oracle/reaction.py", "A2 = (sp.diags(c2 * I) - L).tocsc()", "A2 = (sp.diags(c2 * I) + L).tocsc()")],
+    # IMEX: shift 1/dt instead of 1/(dt mu)
+    "imex_shift": [("oracle/reaction.py", "    c1, c2 = 1.0 / (p.dt * p.mu1), 1.0 / (p.dt * p.mu2)\n    return c1 * (u + p.dt * ru)",
+                    "    c1, c2 = 1.0 / p.dt, 1.0 / p.dt\n    return c1 * (u + p.dt * ru)")],
+    # Schnakenberg noise amplitude
+    "initial_noise": [("oracle/reaction.py", "return (us + 1e-2 * seeded_inputs.uniform_pm1(seed, ijk, stream=0),",
+                       "return (us + 1e-1 * seeded_inputs.uniform_pm1(seed, ijk, stream=0),")],
 }
 
 
@@ -134,6 +171,13 @@ HINTS = {
     "gmres_restart_update": "gmres_dense_random_vs_lu", "ras_keep_shift": "ras_single_subdomain_exact",
     "ras_slab_order": "ras_subdomains_are_band_order_slabs", "initial_state_v": "initial_state_recipe",
     "slab_bounds_ceil": "partition_and_overlap_invariants",
+    "sphere_radius": "sphere_cp_closed_form", "stencil_offset": "semidiscrete_2d_golden",
+    "barycentric_sign": "lagrange_weights_golden", "apply_rows_neighbours": "semidiscrete_2d_golden",
+    "apply_rows_no_extension": "semidiscrete_2d_golden", "laplacian_without_E": "constants_in_kernel",
+    "ghost_index_offset": "delta_h_exact_on_quadratics", "gmres_its_count": "gmres_identity_one_iteration",
+    "gmres_back_substitution": "gmres_dense_random_vs_lu", "fgmres_update_basis": "ras_fgmres_converges",
+    "overlap_26": "overlap_equals_graph_distance_ball", "imex_operator_sign": "schnakenberg_pure_diffusion",
+    "imex_shift": "schnakenberg_constant_state", "initial_noise": "initial_state_recipe",
 }
 
 
