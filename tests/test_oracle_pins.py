@@ -596,3 +596,50 @@ def test_ras_subdomains_are_band_order_slabs():
     dis = disjoint_subdomains(b, 5)
     for s in range(4):
         assert key[dis[s]].max() < key[dis[s + 1]].min()
+
+
+def test_arnoldi_fixed_happy_breakdown():
+    """Reading R6: k GMRES steps stop early only on happy breakdown, and then the iterate is
+    exact on the invariant subspace reached.  A = diag(2, 3, 5, 7): b = 4 e_1 spans a
+    1-dimensional Krylov space (z = b/3 after one column), b = e_0 + e_2 a 2-dimensional
+    one (z = (1/2, 0, 1/5, 0) after two)."""
+    d = np.array([2.0, 3.0, 5.0, 7.0])
+    A = lambda v: d * v  # noqa: E731
+    z = arnoldi_fixed(A, np.array([0.0, 4.0, 0.0, 0.0]), 3)
+    assert np.allclose(z, [0.0, 4.0 / 3.0, 0.0, 0.0], atol=1e-15)
+    z = arnoldi_fixed(A, np.array([1.0, 0.0, 1.0, 0.0]), 4)
+    assert np.allclose(z, [0.5, 0.0, 0.2, 0.0], atol=1e-14)
+
+
+def test_gmres_initial_guess():
+    """x0 is the starting iterate (restarted GMRES; cpm_solve's `u holds x0 on
+    entry`): started at the solution GMRES returns it after 0 iterations; started elsewhere
+    it still converges to the same solution, in fewer iterations from a nearby guess than
+    from zero."""
+    rng = np.random.default_rng(11)
+    M = np.eye(30) * 4.0 + rng.normal(size=(30, 30)) * 0.3
+    xs = rng.normal(size=30)
+    b = M @ xs
+    A = lambda v: M @ v  # noqa: E731
+    x, st = gmres(A, b, x0=xs, restart=10, rtol=1e-12)
+    assert st.iterations == 0 and st.converged and np.array_equal(x, xs)
+    x0, st0 = gmres(A, b, restart=10, rtol=1e-12)
+    x1, st1 = gmres(A, b, x0=xs + 1e-6 * rng.normal(size=30), restart=10, rtol=1e-12)
+    assert st0.converged and st1.converged
+    assert np.allclose(x0, xs, atol=1e-9) and np.allclose(x1, xs, atol=1e-9)
+    assert st1.iterations < st0.iterations
+
+
+def test_rhs_torus_modulation_worked_point():
+    """Reading R10 (the input recipe of configs[2]): f = cos(3 th) sin(2 ph) (1 + sum_q a_q
+    sin(k_q . cp)).  A lattice node on the diagonal x = y of the plane z = 0 outside the
+    torus has cp = ((R + r)/sqrt2, (R + r)/sqrt2, 0), th = 0, ph = pi/4, so f is the
+    modulation itself at that point, evaluated here from the coefficient table."""
+    h = 0.1
+    b = Band(Torus(1.0, 0.4), h)
+    node = np.array([[11, 11, 0]])                     # |x| = 1.556 > R + r: outside, th = 0
+    assert b.index_active(node)[0] >= 0
+    s = 1.4 / math.sqrt(2.0)
+    want = 1.0 + sum(a * math.sin((kx + ky) * s) for a, kx, ky, kz in seeded_inputs.smooth_modulation_coeffs(1))
+    assert abs(want - 1.0) > 1e-3                      # the modulation is visible at this point
+    assert abs(rhs_torus(b, 1, node)[0] - want) < 1e-13

@@ -148,6 +148,21 @@ MUTATIONS = {
     # Schnakenberg noise amplitude
     "initial_noise": [("oracle/reaction.py", "return (us + 1e-2 * seeded_inputs.uniform_pm1(seed, ijk, stream=0),",
                        "return (us + 1e-1 * seeded_inputs.uniform_pm1(seed, ijk, stream=0),")],
+    # interpolation weights where cp falls on a lattice node (t = 0): the unit vector is not substituted
+    "interp_exact_node": [("oracle/interp.py", "    w[hit] = exact[hit].astype(np.float64)\n", "")],
+    # fixed-step Arnoldi: happy breakdown one column short
+    "arnoldi_breakdown_index": [("oracle/krylov.py", "            kk = j + 1\n            break", "            kk = j\n            break")],
+    # Condon-Shortley phase left in (reading R9 removes it)
+    "sph_condon_shortley": [("oracle/sph.py", "P = lpmv(am, l, ct) * (-1.0) ** am", "P = lpmv(am, l, ct)")],
+    # Schnakenberg u-kinetics a + u - u^2 v
+    "reaction_u_terms": [("oracle/reaction.py", "return p.gamma * (p.a - u + u2v), p.gamma * (p.b - u2v)",
+                          "return p.gamma * (p.a + u - u2v), p.gamma * (p.b - u2v)")],
+    # GMRES ignores the initial guess
+    "gmres_x0_ignored": [("oracle/krylov.py", "x = np.zeros(n) if x0 is None else np.array(x0, dtype=np.float64)",
+                          "x = np.zeros(n)")],
+    # the config-2 modulation subtracted instead of added (reading R10)
+    "modulation_sign": [("oracle/problems.py", "mod = mod + a * np.sin(kx * cp[:, 0] + ky * cp[:, 1] + kz * cp[:, 2])",
+                         "mod = mod - a * np.sin(kx * cp[:, 0] + ky * cp[:, 1] + kz * cp[:, 2])")],
 }
 
 
@@ -178,6 +193,9 @@ HINTS = {
     "gmres_back_substitution": "gmres_dense_random_vs_lu", "fgmres_update_basis": "ras_fgmres_converges",
     "overlap_26": "overlap_equals_graph_distance_ball", "imex_operator_sign": "schnakenberg_pure_diffusion",
     "imex_shift": "schnakenberg_constant_state", "initial_noise": "initial_state_recipe",
+    "interp_exact_node": "E_on_lattice_plane_is_selection", "sph_condon_shortley": "real_sph_closed_forms",
+    "reaction_u_terms": "schnakenberg_steady_state", "arnoldi_breakdown_index": "arnoldi_fixed_happy_breakdown",
+    "gmres_x0_ignored": "gmres_initial_guess", "modulation_sign": "rhs_torus_modulation",
 }
 
 
