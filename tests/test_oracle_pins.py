@@ -643,3 +643,29 @@ def test_rhs_torus_modulation_worked_point():
     want = 1.0 + sum(a * math.sin((kx + ky) * s) for a, kx, ky, kz in seeded_inputs.smooth_modulation_coeffs(1))
     assert abs(want - 1.0) > 1e-3                      # the modulation is visible at this point
     assert abs(rhs_torus(b, 1, node)[0] - want) < 1e-13
+
+
+def test_ras_inexact_local_solve_takes_k_steps():
+    """north_star 4 / reading R6: the local solve is exactly k_inner GMRES steps from zero.
+    With one subdomain and no overlap M(r) is that iterate for A z = r, so ||r - A M(r)||
+    equals the least-squares minimum over span{r, A r, ..., A^(k-1) r} (explicit basis,
+    independent lstsq) and is larger than the minimum over k + 1 vectors."""
+    b = Band(Sphere(1.0), 0.16)
+    A = shifted_operator(b, 1.0)
+    r = seeded_inputs.uniform_pm1(4, b.active)
+    k = 5
+    z = RAS(b, A, nsub=1, overlap=0, k_inner=k, local="gmres")(r)
+    res = np.linalg.norm(r - A @ z)
+
+    def krylov_min(m):
+        K = [r / np.linalg.norm(r)]
+        for _ in range(m - 1):
+            v = A @ K[-1]
+            K.append(v / np.linalg.norm(v))
+        AK = np.stack([A @ v for v in K], axis=1)
+        y, *_ = np.linalg.lstsq(AK, r, rcond=None)
+        return np.linalg.norm(r - AK @ y)
+
+    mk, mk1 = krylov_min(k), krylov_min(k + 1)
+    assert mk1 < 0.99 * mk                      # the two are distinguishable
+    assert abs(res - mk) <= 1e-9 * mk

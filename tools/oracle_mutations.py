@@ -160,6 +160,14 @@ MUTATIONS = {
     # GMRES ignores the initial guess
     "gmres_x0_ignored": [("oracle/krylov.py", "x = np.zeros(n) if x0 is None else np.array(x0, dtype=np.float64)",
                           "x = np.zeros(n)")],
+    # RAS: one more inner step than asked for
+    "ras_kinner_plus_1": [("oracle/ras.py", "zj = arnoldi_fixed(lambda v, Aj=Aj: Aj @ v, rj, self.k)",
+                           "zj = arnoldi_fixed(lambda v, Aj=Aj: Aj @ v, rj, self.k + 1)")],
+    # RAS: local problems on the disjoint parts (block Jacobi) although the overlap is grown
+    "ras_local_problem_disjoint": [("oracle/ras.py", "self.over = [grow_overlap(band, d, overlap) for d in self.disjoint]",
+                                    "self.over = [d for d in self.disjoint]")],
+    # stencil base by truncation instead of floor (wrong for negative coordinates)
+    "stencil_trunc": [("oracle/interp.py", "fl = np.floor(s)", "fl = np.trunc(s)")],
     # the config-2 modulation subtracted instead of added (reading R10)
     "modulation_sign": [("oracle/problems.py", "mod = mod + a * np.sin(kx * cp[:, 0] + ky * cp[:, 1] + kz * cp[:, 2])",
                          "mod = mod - a * np.sin(kx * cp[:, 0] + ky * cp[:, 1] + kz * cp[:, 2])")],
@@ -196,6 +204,8 @@ HINTS = {
     "interp_exact_node": "E_on_lattice_plane_is_selection", "sph_condon_shortley": "real_sph_closed_forms",
     "reaction_u_terms": "schnakenberg_steady_state", "arnoldi_breakdown_index": "arnoldi_fixed_happy_breakdown",
     "gmres_x0_ignored": "gmres_initial_guess", "modulation_sign": "rhs_torus_modulation",
+    "ras_kinner_plus_1": "ras_inexact_local_solve_takes_k_steps",
+    "ras_local_problem_disjoint": "ras_stationary_iteration", "stencil_trunc": "reproduce_tricubics",
 }
 
 
