@@ -118,6 +118,23 @@ def test_band_matches_pure_python_triple_loop(surf, h, dist):
     assert b.nA == len(act) and b.nG == len(ghost)
 
 
+def test_band_clipped_by_the_grid_box():
+    """The grid is |i|, |j|, |k| <= M = round(L/h) (oracle/band.py header; cpm_build_band's L):
+    with L = 1 the unit sphere's tube is cut by the box.  Counted here by a plain loop:
+    active nodes are the lattice nodes of the box within lambda of the sphere, the box's
+    faces included."""
+    h, L = 0.2, 1.0
+    b = Band(Sphere(1.0), h, L=L)
+    M = 5
+    lam = math.sqrt(17.0) * h
+    want = {(i, j, k) for i in range(-M, M + 1) for j in range(-M, M + 1) for k in range(-M, M + 1)
+            if abs(math.sqrt((i * h) ** 2 + (j * h) ** 2 + (k * h) ** 2) - 1.0) <= lam}
+    got = set(map(tuple, b.active.tolist()))
+    assert got == want
+    assert any(max(abs(c) for c in n) == M for n in got)          # nodes on the box faces are kept
+    assert len(got) < Band(Sphere(1.0), h).nA                       # and the box does clip the tube
+
+
 def test_band_size_scales_as_h_minus_2():
     n1 = Band(Sphere(1.0), 0.1).nA
     n2 = Band(Sphere(1.0), 0.05).nA

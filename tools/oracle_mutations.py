@@ -168,6 +168,9 @@ MUTATIONS = {
                                     "self.over = [d for d in self.disjoint]")],
     # stencil base by truncation instead of floor (wrong for negative coordinates)
     "stencil_trunc": [("oracle/interp.py", "fl = np.floor(s)", "fl = np.trunc(s)")],
+    # grid box one node short (|i| <= M - 1)
+    "grid_box_clip": [("oracle/band.py", "ihi = [min(M, int(math.ceil(hi[c] / h)) + 1) for c in range(3)]",
+                       "ihi = [min(M - 1, int(math.ceil(hi[c] / h)) + 1) for c in range(3)]")],
     # the config-2 modulation subtracted instead of added (reading R10)
     "modulation_sign": [("oracle/problems.py", "mod = mod + a * np.sin(kx * cp[:, 0] + ky * cp[:, 1] + kz * cp[:, 2])",
                          "mod = mod - a * np.sin(kx * cp[:, 0] + ky * cp[:, 1] + kz * cp[:, 2])")],
@@ -204,7 +207,7 @@ HINTS = {
     "interp_exact_node": "E_on_lattice_plane_is_selection", "sph_condon_shortley": "real_sph_closed_forms",
     "reaction_u_terms": "schnakenberg_steady_state", "arnoldi_breakdown_index": "arnoldi_fixed_happy_breakdown",
     "gmres_x0_ignored": "gmres_initial_guess", "modulation_sign": "rhs_torus_modulation",
-    "ras_kinner_plus_1": "ras_inexact_local_solve_takes_k_steps",
+    "ras_kinner_plus_1": "ras_inexact_local_solve_takes_k_steps", "grid_box_clip": "band_clipped_by_the_grid_box",
     "ras_local_problem_disjoint": "ras_stationary_iteration", "stencil_trunc": "reproduce_tricubics",
 }
 
